@@ -1,0 +1,25 @@
+# Build librotatek.so (sm_100a) and the CPU oracle.
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Xptxas -v --expt-relaxed-constexpr
+PKG := paper_2605_19218_b200
+SRC := $(wildcard $(PKG)/csrc/*.cu)
+OBJ := $(patsubst $(PKG)/csrc/%.cu,build/%.o,$(SRC))
+HDR := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/rotatek.h
+
+all: $(PKG)/librotatek.so oracle/liboracle.so
+
+build/%.o: $(PKG)/csrc/%.cu $(HDR)
+	@mkdir -p build
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
+
+$(PKG)/librotatek.so: $(OBJ)
+	$(NVCC) $(ARCH) -shared -cudart static -o $@.tmp $(OBJ) && mv $@.tmp $@
+
+oracle/liboracle.so: oracle/oracle.c
+	gcc -O2 -fopenmp -fPIC -shared -std=c11 -fno-fast-math -o $@ $< -lm
+
+clean:
+	rm -rf build $(PKG)/librotatek.so oracle/liboracle.so
+
+.PHONY: all clean

@@ -1,0 +1,440 @@
+#!/usr/bin/env python
+"""Benchmark of the RotateK hot path on B200 (contract: see DESIGN.md "Measurement").
+
+    python bench.py [--gpus N --steps K --warmup W] [--config llava_b32] [--layers L]
+    python bench.py --impl reference ...        (the fp64 CPU oracle, bounded sample)
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Headline (BASELINE.json metric): sparse-channel decode attention us/layer and HBM GB/s.
+One timed step = one decode pass (Alg. 2, all query heads, one rotatek_decode_attn
+launch per layer) over L distinct layer caches of the workload, captured in a CUDA
+graph.  `value` = algorithmic decode bytes of all ranks / max-over-ranks step time.
+The full hot path (calibrate + compress + decode per layer, every SURVEY §8(a) row) is
+timed as well and reported under "full_step"; "e2e" runs that full path from pinned
+host buffers with the host<->device copies inside the timed region.
+Multi-GPU: weak scaling, each rank owns its own batch of units (b x kv-head); no
+collective on the data path (units are independent).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from workload import CONFIGS, compress_bytes, decode_bytes, decode_flops, make_workload  # noqa: E402
+
+METRIC = json.load(open(os.path.join(ROOT, "BASELINE.json")))["metric"]
+NOMINAL_HBM_GBS = 8000.0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="llava_b32")
+    ap.add_argument("--layers", type=int, default=4)
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 generic, 2 fast")
+    ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--skip-full", action="store_true")
+    ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d["hbm_gbs"], "measured", d
+    return 6650.0, "fallback (B200_PROFILING.md)", {}
+
+
+def rank_units(cfg, rank):
+    return list(range(rank * cfg.units, (rank + 1) * cfg.units))
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_decode_sample(cfg, seconds, max_units=None):
+    """Time the fp64 oracle's Alg. 2 on a bounded sample of units (inputs prepared
+    untimed, oracle calibrate for the caches).  Returns (GB/s in the metric's bytes,
+    sample description, cores, seconds spent)."""
+    from oracle import oracle as orc
+    n_units = max(1, min(cfg.units, max_units or 64))
+    w = make_workload(cfg, units=range(n_units), threads=os.cpu_count() or 8)
+    cal = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
+    Kt = orc.quantize(orc.compress(w["K"].f64(), cal["R"]), cfg.dtype)
+    args = (w["q"].f64(), Kt, w["V"].f64(), cal["R"], cal["dmu"], w["Ktext"].f64(),
+            w["Vtext"].f64())
+    sub = cfg.with_(batch=1, h_kv=n_units)
+    reps, t0 = 0, time.perf_counter()
+    while True:
+        orc.decode(*args)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds:
+            break
+    gbs = decode_bytes(sub) * reps / el / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return gbs, f"{n_units} of {cfg.units} units of {cfg.name}, {reps} decode passes", cores, el
+
+
+def run_reference(args):
+    """--impl reference: the oracle as it stands, on the host cores (rank 0 only)."""
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    cfg = CONFIGS[args.config]
+    from oracle import oracle as orc
+    n_units = max(1, min(cfg.units, 32))
+    w = make_workload(cfg, units=range(n_units), threads=os.cpu_count() or 8)
+    cal = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
+    Kt = orc.quantize(orc.compress(w["K"].f64(), cal["R"]), cfg.dtype)
+    dargs = (w["q"].f64(), Kt, w["V"].f64(), cal["R"], cal["dmu"], w["Ktext"].f64(),
+             w["Vtext"].f64())
+    for _ in range(args.warmup):
+        orc.decode(*dargs)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        orc.decode(*dargs)
+        times.append(time.perf_counter() - t0)
+    sub = cfg.with_(batch=1, h_kv=n_units)
+    tot = sum(times)
+    gbs = decode_bytes(sub) * len(times) / tot / 1e9
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(gbs, 4), "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * tot / len(times), 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": cfg.name, "units": cfg.units, "sample_units": n_units,
+                   "n_vis": cfg.n_vis, "n_text": cfg.n_text, "head_dim": cfg.head_dim,
+                   "rank": cfg.rank, "group": cfg.group},
+        "cpu_baseline": {"value": round(gbs, 4), "unit": "GB/s", "cores": cores,
+                         "kind": "oracle",
+                         "sample": f"{n_units} of {cfg.units} units, one decode pass per step"},
+        "e2e": {"value": round(gbs, 4), "unit": "GB/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- clocks
+class Clocks:
+    def __init__(self, gpu_index):
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.proc = None
+        self.gpu = gpu_index
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}",
+                                          f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                rows.append(parts)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_19218_b200 as rk
+
+    world, rank, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    L = args.layers
+    peak_gbs, peak_kind, _ = peaks()
+
+    # ---------------- inputs: layer 0 drawn on the host (per-unit seeded, this rank's
+    # units); layers 1..L-1 are distinct device buffers (unit axis rolled).
+    t_gen = time.perf_counter()
+    host = make_workload(cfg, units=rank_units(cfg, rank), threads=os.cpu_count() or 8)
+    t_gen = time.perf_counter() - t_gen
+
+    def to_dev(t):
+        x = np.ascontiguousarray(t.bits)
+        if t.dtype == "bf16":
+            x = torch.from_numpy(x.view(np.int16)).view(torch.bfloat16)
+        else:
+            x = torch.from_numpy(x)
+        return x.to(dev)
+
+    base = {k: to_dev(host[k]) for k in ("K", "V", "Ktext", "Vtext", "Qw", "q")}
+    layers = []
+    for l in range(L):
+        sh = (7 * l) % cfg.units
+        layers.append({k: torch.roll(v, shifts=sh, dims=0).contiguous() if l else v
+                       for k, v in base.items()})
+    # prefill (calibrate + compress) -> the compressed caches the decode step reads
+    for ly in layers:
+        cal = rk.calibrate(ly["K"], ly["Qw"], cfg.rank)
+        ly["R"], ly["dmu"], ly["info"] = cal["R"], cal["dmu"], cal["info"]
+        ly["Kc"] = rk.compress_kv(ly["K"], ly["R"])
+        ly["out"] = torch.empty((cfg.units, cfg.group, cfg.head_dim), dtype=torch.float32,
+                                device=dev)
+    torch.cuda.synchronize()
+    bad_info = int(sum((ly["info"] != 0).sum().item() for ly in layers))
+
+    stream = torch.cuda.Stream(device=dev)
+    dims = rk.make_dims(cfg.units, cfg.group, cfg.head_dim, cfg.rank, cfg.n_vis, cfg.n_text, 0,
+                        rk.BF16 if cfg.dtype == "bf16" else rk.F32)
+    with torch.cuda.stream(stream):
+        ws = torch.zeros(rk.workspace_bytes(dims, rk.OP_DECODE), dtype=torch.uint8, device=dev)
+
+    def decode_step():
+        for ly in layers:
+            rk.decode_attn(ly["q"], ly["Kc"], ly["V"], ly["R"], ly["dmu"], ly["Ktext"],
+                           ly["Vtext"], out=ly["out"], ws=ws, kernel=args.kernel, stream=stream)
+
+    graph = None
+    stream.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(stream):
+        decode_step()
+        if not args.no_graph:
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph, stream=stream):
+                decode_step()
+    torch.cuda.synchronize()
+
+    def run_step():
+        if graph is not None:
+            with torch.cuda.stream(stream):
+                graph.replay()
+        else:
+            decode_step()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # ---------------- timed region A: decode steps
+    for _ in range(args.warmup):
+        run_step()
+    barrier()
+    clocks = Clocks(local)
+    with clocks:
+        ev0 = torch.cuda.Event(enable_timing=True)
+        ev1 = torch.cuda.Event(enable_timing=True)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            run_step()
+        ev1.record(stream)
+        barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    if world > 1:
+        t = torch.tensor([ms_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+    us_layer = 1e3 * ms_step / L
+    bytes_layer = decode_bytes(cfg)
+    achieved = bytes_layer / (us_layer * 1e-6) / 1e9          # per-launch GB/s (this rank)
+    value = world * bytes_layer * L / (ms_step * 1e-3) / 1e9   # whole job
+
+    # ---------------- timed region B: the full hot path per layer (rows 1-8), phase events
+    full = None
+    if not args.skip_full:
+        calws = torch.zeros(rk.workspace_bytes(
+            rk.make_dims(cfg.units, cfg.group, cfg.head_dim, cfg.rank, cfg.n_vis, 0,
+                         cfg.q_window, dims.dtype), rk.OP_CALIBRATE), dtype=torch.uint8,
+            device=dev)
+        n_full = max(2, min(5, args.steps))
+        phase_ms = {"calibrate": 0.0, "compress": 0.0, "decode": 0.0}
+        for it in range(1 + n_full):
+            evs = []
+            with torch.cuda.stream(stream):
+                for ly in layers:
+                    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                    e[0].record(stream)
+                    cal = rk.calibrate(ly["K"], ly["Qw"], cfg.rank, ws=calws, stream=stream)
+                    e[1].record(stream)
+                    rk.compress_kv(ly["K"], cal["R"], out=ly["Kc"], stream=stream)
+                    e[2].record(stream)
+                    rk.decode_attn(ly["q"], ly["Kc"], ly["V"], cal["R"], cal["dmu"], ly["Ktext"],
+                                   ly["Vtext"], out=ly["out"], ws=ws, stream=stream)
+                    e[3].record(stream)
+                    evs.append(e)
+            torch.cuda.synchronize()
+            if it == 0:
+                continue  # warm-up pass
+            for e in evs:
+                phase_ms["calibrate"] += e[0].elapsed_time(e[1])
+                phase_ms["compress"] += e[1].elapsed_time(e[2])
+                phase_ms["decode"] += e[2].elapsed_time(e[3])
+        per_layer_us = {k: round(1e3 * v / (n_full * L), 2) for k, v in phase_ms.items()}
+        step_ms = sum(phase_ms.values()) / n_full
+        cb = compress_bytes(cfg)
+        full = {"ms_per_step": round(step_ms, 3), "layers": L,
+                "us_per_layer": per_layer_us,
+                "prefill_tokens_per_s": round(cfg.units * cfg.n_vis /
+                                              ((per_layer_us["calibrate"] + per_layer_us["compress"]) * 1e-6), 1),
+                "compress_gbs_1pass_bytes": round(cb / (per_layer_us["compress"] * 1e-6) / 1e9, 1)}
+
+    # ---------------- e2e: full path from pinned host buffers, H2D/D2H inside the timed region
+    e2e = None
+    if not args.skip_e2e:
+        names = ("K", "V", "Ktext", "Vtext", "Qw", "q")
+        pinned = {k: to_dev(host[k]).cpu().pin_memory() for k in names}
+        dbuf = {k: torch.empty_like(pinned[k], device=dev) for k in names}
+        out_h = torch.empty((cfg.units, cfg.group, cfg.head_dim), dtype=torch.float32).pin_memory()
+        Kc_d = torch.empty_like(layers[0]["Kc"])
+        calws2 = torch.zeros(rk.workspace_bytes(
+            rk.make_dims(cfg.units, cfg.group, cfg.head_dim, cfg.rank, cfg.n_vis, 0,
+                         cfg.q_window, dims.dtype), rk.OP_CALIBRATE), dtype=torch.uint8,
+            device=dev)
+        h2d = sum(v.numel() * v.element_size() for v in pinned.values())
+        d2h = out_h.numel() * 4
+
+        def e2e_step():
+            with torch.cuda.stream(stream):
+                for k in names:
+                    dbuf[k].copy_(pinned[k], non_blocking=True)
+                cal = rk.calibrate(dbuf["K"], dbuf["Qw"], cfg.rank, ws=calws2, stream=stream)
+                rk.compress_kv(dbuf["K"], cal["R"], out=Kc_d, stream=stream)
+                o = rk.decode_attn(dbuf["q"], Kc_d, dbuf["V"], cal["R"], cal["dmu"],
+                                   dbuf["Ktext"], dbuf["Vtext"], ws=ws, stream=stream)
+                out_h.copy_(o, non_blocking=True)
+
+        e2e_step()
+        barrier()
+        n_e2e = max(2, min(5, args.steps))
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(n_e2e):
+            e2e_step()
+        a1.record(stream)
+        barrier()
+        e_ms = a0.elapsed_time(a1) / n_e2e
+        if world > 1:
+            t = torch.tensor([e_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            e_ms = float(t.item())
+        e2e = {"value": round(world * bytes_layer / (e_ms * 1e-3) / 1e9, 3), "unit": "GB/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": round(e_ms, 3),
+               "path": "pinned host -> H2D -> calibrate -> compress -> decode -> D2H (1 layer)"}
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    cpu = None
+    if world == 1 and not args.skip_cpu:
+        gbs, sample, cores, el = oracle_decode_sample(cfg, args.cpu_seconds)
+        cpu = {"value": round(gbs, 4), "unit": "GB/s", "cores": cores, "kind": "oracle",
+               "sample": sample, "seconds": round(el, 2)}
+
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        tr = json.load(open(tp)).get(cfg.name)
+        if tr:
+            traffic = tr.get("dram_bytes_per_launch")
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "GB/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": cfg.dtype, "data": "synthetic (seeded nat distribution, SURVEY §8(d))",
+        "config": {"workload": cfg.name, "batch_per_gpu": cfg.batch, "global_batch": cfg.batch * world,
+                   "h_kv": cfg.h_kv, "group": cfg.group, "units_per_gpu": cfg.units,
+                   "head_dim": cfg.head_dim, "rank": cfg.rank, "n_vis": cfg.n_vis,
+                   "n_text": cfg.n_text, "layers_timed": L,
+                   "parallelism": f"units sharded by (batch x kv head), weak, {world} GPU(s)",
+                   "l2": "inputs larger than L2 (decode bytes/layer %.0f MB x %d layers > 126 MB)"
+                         % (bytes_layer / 1e6, L),
+                   "cuda_graph": graph is not None},
+        "us_per_layer": round(us_layer, 3),
+        "pct_of_8tbs": round(100 * achieved / NOMINAL_HBM_GBS, 2),
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak_gbs,
+                     "unit": "GB/s", "frac": round(achieved / peak_gbs, 4), "traffic": traffic,
+                     "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_launch": bytes_layer,
+                     "kernel": "rotatek decode (fast TMA-bulk warp-streaming kernel)"},
+        "decode_tflops": round(decode_flops(cfg) / (us_layer * 1e-6) / 1e12, 3),
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "full_step": full,
+        "clocks": clocks.summary(),
+        "gpu_launches": args.steps * L,
+        "calibrate_info_nonzero": bad_info,
+        "host_gen_s": round(t_gen, 1),
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,201 @@
+/*
+ * rotatek.h -- C ABI of librotatek.so, the B200 (sm_100a) hot path of RotateK
+ * (arxiv 2605.19218, "rotation-based structured Key-channel pruning for VLM
+ * KV caches").
+ *
+ * The three calls follow the paper's problem statement:
+ * compress the Keys K in R^{N x d} of N visual tokens to r < d channels with
+ * minimal perturbation of q_t K^T.
+ *   rotatek_calibrate    = Alg. 1 (alg:rotatek-prefill) lines 1-5
+ *                          and the basis choice with an exact
+ *                          eigendecomposition (batched Jacobi), then top-r
+ *                          select and delta_mu = (I - R_r R_r^T) mu.
+ *   rotatek_compress_kv  = Alg. 1 line 14: K~ = K R_r, "stored in place of K".
+ *   rotatek_decode_attn  = Alg. 2 (alg:rotatek-decode) for every
+ *                          query head: q~ = q R_r, b = q . delta_mu,
+ *                          scores (q~ K~^T + b)/sqrt(d) over the visual tokens
+ *                          and q K_pt^T / sqrt(d) over the full-d prompt/text
+ *                          tokens, softmax over the concatenation, weighted sum
+ *                          of full-d values (App. C).
+ *
+ * Conventions for every call
+ *   - A "unit" is one (batch element, KV head): u = b * H_kv + h_kv.  All
+ *     per-unit tensors are laid out [U, ...] row-major and contiguous, so a
+ *     shard of units is a pointer offset (u0 * per-unit stride).
+ *   - Query head h of unit u is g = h - u*G (h_kv = floor(h / G)).
+ *   - All tensor pointers are DEVICE pointers, 16-byte aligned.  Buffers are
+ *     owned by the caller; the library allocates nothing and keeps no state
+ *     between calls.
+ *   - Every call validates its arguments on the host, then only ENQUEUES work
+ *     on `stream`: no synchronisation, no allocation, CUDA-graph capturable.
+ *     Numerical problems are reported per unit on the device through `info`.
+ *   - No C++ exception crosses the ABI.  A non-OK status leaves the outputs
+ *     untouched; rotatek_last_error() gives a thread-local detail string.
+ *   - Workspaces: ask rotatek_workspace_bytes().  The workspace must be
+ *     ZERO-FILLED once before its first use (e.g. cudaMemset / torch.zeros);
+ *     every call leaves its counter region zeroed again, so the same
+ *     workspace can be reused (and graph-replayed) without re-zeroing.
+ *     Concurrent calls on different streams need different workspaces.
+ */
+#ifndef ROTATEK_H_
+#define ROTATEK_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ROTATEK_ABI_VERSION 1
+
+typedef struct CUstream_st* rotatek_stream_t; /* == cudaStream_t; NULL = legacy default */
+
+typedef enum {
+  ROTATEK_OK = 0,
+  ROTATEK_ERR_NULL = 1,        /* a required pointer is NULL                          */
+  ROTATEK_ERR_DIMS = 2,        /* U<1, G<1, N<1, M<0, W<0, r not in [1,d], d invalid  */
+  ROTATEK_ERR_ALIGN = 3,       /* a pointer is not 16-byte aligned                    */
+  ROTATEK_ERR_WORKSPACE = 4,   /* workspace NULL or smaller than rotatek_workspace_bytes */
+  ROTATEK_ERR_UNSUPPORTED = 5, /* no kernel for this (d, r, dtype) combination        */
+  ROTATEK_ERR_CUDA = 6         /* a kernel launch failed (see rotatek_last_error)     */
+} rotatek_status;
+
+typedef enum { ROTATEK_BF16 = 0, ROTATEK_F32 = 1 } rotatek_dtype;
+
+/* calibrate flags */
+enum {
+  ROTATEK_CENTER = 1u << 0,       /* subtract the per-channel mean mu.  Off:
+                                     mu = 0, C = K^T K (north_star's literal wording)  */
+  ROTATEK_QUERY_WEIGHT = 1u << 1, /* C_q = (sigma sigma^T) (.) C.  Off (or
+                                     W == 0): sigma == 1, the K-only PCA arm   */
+  ROTATEK_EIG_FP32 = 1u << 2,     /* bf16 caches only: run the Jacobi eigensolver in fp32
+                                     (faster; projector error ~1e-4, which can exceed
+                                     the 2e-3 end-to-end gate on some data).  Default:
+                                     fp64 Jacobi (projector error ~1e-7)               */
+  ROTATEK_DEFAULT_FLAGS = (1u << 0) | (1u << 1)
+};
+
+typedef enum { ROTATEK_OP_CALIBRATE = 0, ROTATEK_OP_DECODE = 1 } rotatek_op;
+
+typedef struct {
+  int32_t units;        /* U = B * H_kv  (>= 1)                                         */
+  int32_t group;        /* G = H_q / H_kv (>= 1): 1 (LLaVA-NeXT MHA), 7 (Qwen2.5-VL)    */
+  int32_t head_dim;     /* d: 16..256, multiple of 16                                   */
+  int32_t rank;         /* r kept rotated channels: 1 <= r <= d                          */
+  int32_t n_vis;        /* N >= 1 visual tokens per unit (after token pruning)          */
+  int32_t n_text;       /* M >= 0 full-d prompt/text/generated tokens per unit          */
+  int32_t q_window;     /* W >= 0 recent prefill queries per query head (paper: 32)     */
+  rotatek_dtype dtype;  /* element type of K, V, Qw, q, K~, K_text, V_text              */
+} rotatek_dims;
+
+/* Bytes of device workspace `op` needs for these dims (0 if dims are invalid). */
+size_t rotatek_workspace_bytes(const rotatek_dims* dims, rotatek_op op);
+
+/*
+ * Alg. 1 steps 1-5 plus the basis choice and delta_mu:
+ *   sigma_j = ||Q_W[:, j]||_2 over the G*W window rows of the unit
+ *   mu      = (1/N) sum_n K_n                     (ROTATEK_CENTER, else 0)
+ *   C       = (K - mu)^T (K - mu)                 (no 1/N)
+ *   C_q     = (sigma sigma^T) (.) C               (ROTATEK_QUERY_WEIGHT, else C)
+ *   C_q     = R diag(lambda) R^T                  (batched parallel Jacobi)
+ *   keep    = the r largest lambda, ties -> lower solver index
+ *   R_r     = R[:, keep] in ascending index order
+ *   dmu     = mu - R_r (R_r^T mu), computed in fp64 from the STORED R_r
+ * Inputs
+ *   K   [U, N, d]      dims->dtype
+ *   Qw  [U, G, W, d]   dims->dtype; may be NULL iff W == 0
+ * Outputs (caller-allocated; nullable ones may be NULL)
+ *   R        [U, d, r] fp32: RNE of the solver's eigenvectors to fp32.  Compress
+ *            and decode must be given this same R (K~, q~ and delta_mu are all
+ *            built from the stored values).
+ *   dmu      [U, d] fp32 (zeros when !ROTATEK_CENTER)
+ *   eigvals  [U, d] fp32, all eigenvalues in solver order (nullable).  The
+ *            select step ranks exactly these fp32 values.
+ *   keep_mask[U, ceil(d/32)] uint32, bit i%32 of word i/32 <=> channel i kept (nullable)
+ *   keep_idx [U, r] int32 ascending (nullable)
+ *   R_full   [U, d, d] fp32 full eigenbasis, columns in solver order (nullable; tests)
+ *   info     [U] int32: 0 ok; s > 0 not converged after s sweeps (results are
+ *            still written); -1 non-finite input (R, dmu zero-filled, mask 0,
+ *            idx -1) (nullable)
+ * Errors: NULL, DIMS, ALIGN, WORKSPACE, UNSUPPORTED (d > 256), CUDA.
+ */
+rotatek_status rotatek_calibrate(const rotatek_dims* dims, uint32_t flags, const void* K,
+                                 const void* Qw, float* R, float* dmu, float* eigvals,
+                                 uint32_t* keep_mask, int32_t* keep_idx, float* R_full,
+                                 int32_t* info, void* workspace, size_t workspace_bytes,
+                                 rotatek_stream_t stream);
+
+/*
+ * Alg. 1 line 14: K~ = RNE_dtype(K R_r), over the UNCENTERED K.
+ *   K      [U, N, d]  dims->dtype
+ *   R      [U, d, r]  fp32 as written by rotatek_calibrate
+ *   K_comp [U, N, r]  dims->dtype (output).  V is not touched: values keep
+ *                     all d channels (App. C).
+ * Errors: NULL, DIMS, ALIGN, UNSUPPORTED, CUDA.
+ */
+rotatek_status rotatek_compress_kv(const rotatek_dims* dims, const void* K, const float* R,
+                                   void* K_comp, rotatek_stream_t stream);
+
+/*
+ * Alg. 2 for all U*G query heads in one launch:
+ *   q~ = q R_r ; b = q . dmu
+ *   s_vis[n] = (q~ . K~[n] + b) * scale          n < N   (rotated, r channels)
+ *   s_pt[m]  = (q . K_text[m]) * scale           m < M   (full d channels)
+ *   out = softmax([s_vis; s_pt]) [V; V_text]     (fp32 accumulation, exact
+ *         online-softmax split-K merge, epsilon = 0)
+ *   q       [U, G, d]  dims->dtype   (== [B, H_q, d] since h = u*G + g)
+ *   K_comp  [U, N, r]  dims->dtype
+ *   V       [U, N, d]  dims->dtype
+ *   R       [U, d, r]  fp32 (the calibrate output)
+ *   dmu     [U, d]     fp32 (may be NULL: b = 0)
+ *   K_text, V_text [U, M, d] dims->dtype, NULL iff M == 0
+ *   softmax_scale <= 0 selects 1/sqrt(d) -- NOT 1/sqrt(r) (Alg. 2 line 3)
+ *   out     [U, G, d]  fp32 (output)
+ * Errors: NULL, DIMS, ALIGN, WORKSPACE, CUDA.
+ */
+rotatek_status rotatek_decode_attn(const rotatek_dims* dims, const void* q, const void* K_comp,
+                                   const void* V, const float* R, const float* dmu,
+                                   const void* K_text, const void* V_text, float softmax_scale,
+                                   float* out, void* workspace, size_t workspace_bytes,
+                                   rotatek_stream_t stream);
+
+/*
+ * Same as rotatek_decode_attn with an explicit split-K factor over the token
+ * axis (splits <= 0: automatic, sized to fill the 148 SMs).  The result is
+ * the same up to fp32 re-association for every split count (App. C "standard
+ * online-softmax merge").  `kernel` forces the implementation:
+ * 0 auto, 1 the generic kernel (any d, r, G), 2 the TMA-pipelined kernel
+ * (returns UNSUPPORTED if the shape has none).  Used by tests and benches.
+ */
+rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dims, const void* q,
+                                      const void* K_comp, const void* V, const float* R,
+                                      const float* dmu, const void* K_text, const void* V_text,
+                                      float softmax_scale, float* out, void* workspace,
+                                      size_t workspace_bytes, int32_t splits, int32_t kernel,
+                                      rotatek_stream_t stream);
+
+/*
+ * The top-r select + compaction step on its own (the selection half of
+ * rotatek_calibrate, exposed so that it can be checked bit-exactly on given
+ * eigenvalue arrays, including adversarial ties):
+ *   eigvals  [U, d] fp32 device      keep = r largest, ties -> lower index
+ *   keep_mask[U, ceil(d/32)] uint32   keep_idx [U, r] int32 ascending
+ *   info     [U] int32: 0, or -1 if a NaN is present (mask 0, idx -1)
+ * Errors: NULL, DIMS, ALIGN, CUDA.
+ */
+rotatek_status rotatek_select_topr(int32_t units, int32_t head_dim, int32_t rank,
+                                   const float* eigvals, uint32_t* keep_mask, int32_t* keep_idx,
+                                   int32_t* info, rotatek_stream_t stream);
+
+/* Number of kernel launches the last successful call on this thread enqueued. */
+int rotatek_last_launch_count(void);
+
+const char* rotatek_status_string(rotatek_status status);
+const char* rotatek_last_error(void); /* thread-local detail for the last non-OK return */
+int rotatek_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* ROTATEK_H_ */

@@ -1,0 +1,9 @@
+"""B200-native (sm_100a) hot path of RotateK (arxiv 2605.19218).
+
+librotatek.so implements Alg. 1 (calibrate + compress) and Alg. 2 (decode) in
+hand-written CUDA; this package is only its ctypes binding (rotatek.py).
+"""
+from .rotatek import (calibrate, compress_kv, decode_attn, select_topr, workspace,  # noqa: F401
+                      workspace_bytes, make_dims, lib, last_launch_count, RotateKError,
+                      BF16, F32, CENTER, QUERY_WEIGHT, EIG_FP32, DEFAULT_FLAGS,
+                      OP_CALIBRATE, OP_DECODE, KERNEL_AUTO, KERNEL_GENERIC, KERNEL_FAST)

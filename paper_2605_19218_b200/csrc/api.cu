@@ -1,0 +1,191 @@
+// api.cu -- the C ABI of librotatek.so (declared in include/rotatek.h).
+// Host-side validation, workspace carving and kernel launches; never synchronises.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+
+#include "../../include/rotatek.h"
+#include "internal.h"
+
+namespace {
+
+thread_local char g_err[512] = "";
+thread_local int g_launches = 0;
+
+rotatek_status fail(rotatek_status s, const char* fmt, const char* what = "") {
+  snprintf(g_err, sizeof(g_err), fmt, what);
+  return s;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+rotatek_status check_dims(const rotatek_dims* dm) {
+  if (!dm) return fail(ROTATEK_ERR_NULL, "dims is NULL");
+  if (dm->units < 1) return fail(ROTATEK_ERR_DIMS, "units must be >= 1");
+  if (dm->group < 1) return fail(ROTATEK_ERR_DIMS, "group must be >= 1");
+  if (dm->head_dim < 16 || dm->head_dim > 256 || dm->head_dim % 16 != 0)
+    return fail(ROTATEK_ERR_DIMS, "head_dim must be a multiple of 16 in [16, 256]");
+  if (dm->rank < 1 || dm->rank > dm->head_dim) return fail(ROTATEK_ERR_DIMS, "rank must be in [1, head_dim]");
+  if (dm->n_vis < 1) return fail(ROTATEK_ERR_DIMS, "n_vis must be >= 1 (empty visual segment)");
+  if (dm->n_text < 0) return fail(ROTATEK_ERR_DIMS, "n_text must be >= 0");
+  if (dm->q_window < 0) return fail(ROTATEK_ERR_DIMS, "q_window must be >= 0");
+  if (dm->dtype != ROTATEK_BF16 && dm->dtype != ROTATEK_F32) return fail(ROTATEK_ERR_DIMS, "bad dtype");
+  return ROTATEK_OK;
+}
+
+rotatek_status launched(int rc, int* count) {
+  if (rc == -2) return fail(ROTATEK_ERR_UNSUPPORTED, "no kernel for this shape");
+  if (rc < 0) {
+    cudaError_t e = cudaGetLastError();
+    return fail(ROTATEK_ERR_CUDA, "kernel launch failed: %s", cudaGetErrorString(e));
+  }
+  *count += rc;
+  return ROTATEK_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rotatek_abi_version(void) { return ROTATEK_ABI_VERSION; }
+const char* rotatek_last_error(void) { return g_err; }
+int rotatek_last_launch_count(void) { return g_launches; }
+
+const char* rotatek_status_string(rotatek_status s) {
+  switch (s) {
+    case ROTATEK_OK: return "ROTATEK_OK";
+    case ROTATEK_ERR_NULL: return "ROTATEK_ERR_NULL";
+    case ROTATEK_ERR_DIMS: return "ROTATEK_ERR_DIMS";
+    case ROTATEK_ERR_ALIGN: return "ROTATEK_ERR_ALIGN";
+    case ROTATEK_ERR_WORKSPACE: return "ROTATEK_ERR_WORKSPACE";
+    case ROTATEK_ERR_UNSUPPORTED: return "ROTATEK_ERR_UNSUPPORTED";
+    case ROTATEK_ERR_CUDA: return "ROTATEK_ERR_CUDA";
+  }
+  return "ROTATEK_ERR_UNKNOWN";
+}
+
+size_t rotatek_workspace_bytes(const rotatek_dims* dm, rotatek_op op) {
+  if (check_dims(dm) != ROTATEK_OK) return 0;
+  if (op == ROTATEK_OP_CALIBRATE)
+    return rk::calib_ws_layout(dm->units, dm->head_dim, dm->n_vis, true, nullptr, nullptr);
+  if (op == ROTATEK_OP_DECODE)
+    return rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->n_vis, dm->n_text, nullptr,
+                                nullptr);
+  return 0;
+}
+
+rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const void* K,
+                                 const void* Qw, float* R, float* dmu, float* eigvals,
+                                 uint32_t* keep_mask, int32_t* keep_idx, float* R_full,
+                                 int32_t* info, void* workspace, size_t workspace_bytes,
+                                 rotatek_stream_t stream) {
+  g_launches = 0;
+  rotatek_status s = check_dims(dm);
+  if (s != ROTATEK_OK) return s;
+  const int U = dm->units, G = dm->group, d = dm->head_dim, r = dm->rank, N = dm->n_vis,
+            W = dm->q_window;
+  const bool bf16 = dm->dtype == ROTATEK_BF16;
+  const bool weight = (flags & ROTATEK_QUERY_WEIGHT) && W > 0;
+  const bool center = (flags & ROTATEK_CENTER) != 0;
+  const bool fp64 = !bf16 || !(flags & ROTATEK_EIG_FP32);
+  if (!K || !R || !dmu) return fail(ROTATEK_ERR_NULL, "K, R and dmu are required");
+  if (W > 0 && !Qw) return fail(ROTATEK_ERR_DIMS, "Qw is NULL but q_window > 0");
+  if (d > 128) return fail(ROTATEK_ERR_UNSUPPORTED, "calibrate supports head_dim <= 128");
+  const void* ptrs[] = {K, Qw, R, dmu, eigvals, keep_mask, keep_idx, R_full, info, workspace};
+  for (const void* p : ptrs)
+    if (p && !aligned16(p)) return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
+  rk::CalibWs ws;
+  const size_t need = rk::calib_ws_layout(U, d, N, true, workspace, &ws);
+  if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int n = 0;
+  if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
+  if ((s = launched(rk::launch_cov(U, N, d, bf16, K, ws, st), &n))) return s;
+  if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
+  if ((s = launched(rk::launch_jacobi(U, d, fp64, ws, st), &n))) return s;
+  if ((s = launched(rk::launch_select_gather(U, d, r, fp64, bf16, center, ws, R, dmu, eigvals,
+                                             keep_mask, keep_idx, R_full, info, st), &n)))
+    return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
+rotatek_status rotatek_compress_kv(const rotatek_dims* dm, const void* K, const float* R,
+                                   void* K_comp, rotatek_stream_t stream) {
+  g_launches = 0;
+  rotatek_status s = check_dims(dm);
+  if (s != ROTATEK_OK) return s;
+  if (!K || !R || !K_comp) return fail(ROTATEK_ERR_NULL, "K, R and K_comp are required");
+  if (!aligned16(K) || !aligned16(R) || !aligned16(K_comp))
+    return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
+  const int d = dm->head_dim, r = dm->rank;
+  if (((size_t)d * r + 64 * (size_t)d) * 4 > 227 * 1024)
+    return fail(ROTATEK_ERR_UNSUPPORTED, "compress: d*r too large");
+  int n = 0;
+  if ((s = launched(rk::launch_compress(dm->units, dm->n_vis, d, r, dm->dtype == ROTATEK_BF16, K, R,
+                                        K_comp, reinterpret_cast<cudaStream_t>(stream)), &n)))
+    return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
+rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dm, const void* q, const void* K_comp,
+                                      const void* V, const float* R, const float* dmu,
+                                      const void* K_text, const void* V_text, float softmax_scale,
+                                      float* out, void* workspace, size_t workspace_bytes,
+                                      int32_t splits, int32_t kernel, rotatek_stream_t stream) {
+  g_launches = 0;
+  rotatek_status s = check_dims(dm);
+  if (s != ROTATEK_OK) return s;
+  const int M = dm->n_text;
+  if (!q || !K_comp || !V || !R || !out) return fail(ROTATEK_ERR_NULL, "q, K_comp, V, R, out are required");
+  if (M > 0 && (!K_text || !V_text)) return fail(ROTATEK_ERR_NULL, "K_text/V_text required when n_text > 0");
+  const void* ptrs[] = {q, K_comp, V, R, dmu, K_text, V_text, out, workspace};
+  for (const void* p : ptrs)
+    if (p && !aligned16(p)) return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
+  rk::DecodeWs ws;
+  const size_t need = rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->n_vis, M,
+                                           workspace, &ws);
+  if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
+  if (kernel < 0 || kernel > 2) return fail(ROTATEK_ERR_DIMS, "kernel must be 0, 1 or 2");
+  rk::DecodeArgs a;
+  a.U = dm->units; a.G = dm->group; a.d = dm->head_dim; a.r = dm->rank; a.N = dm->n_vis; a.M = M;
+  a.bf16 = dm->dtype == ROTATEK_BF16;
+  a.q = q; a.Kc = K_comp; a.V = V; a.R = R; a.dmu = dmu;
+  a.Kt = M > 0 ? K_text : nullptr; a.Vt = M > 0 ? V_text : nullptr;
+  a.scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf((float)dm->head_dim);
+  a.out = out;
+  int n = 0;
+  if ((s = launched(rk::launch_decode(a, ws, splits, kernel, reinterpret_cast<cudaStream_t>(stream)), &n)))
+    return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
+rotatek_status rotatek_decode_attn(const rotatek_dims* dm, const void* q, const void* K_comp,
+                                   const void* V, const float* R, const float* dmu,
+                                   const void* K_text, const void* V_text, float softmax_scale,
+                                   float* out, void* workspace, size_t workspace_bytes,
+                                   rotatek_stream_t stream) {
+  return rotatek_decode_attn_ex(dm, q, K_comp, V, R, dmu, K_text, V_text, softmax_scale, out,
+                                workspace, workspace_bytes, 0, 0, stream);
+}
+
+rotatek_status rotatek_select_topr(int32_t units, int32_t head_dim, int32_t rank,
+                                   const float* eigvals, uint32_t* keep_mask, int32_t* keep_idx,
+                                   int32_t* info, rotatek_stream_t stream) {
+  g_launches = 0;
+  if (units < 1 || head_dim < 1 || head_dim > 256 || rank < 1 || rank > head_dim)
+    return fail(ROTATEK_ERR_DIMS, "bad select dims");
+  if (!eigvals || !keep_mask || !keep_idx) return fail(ROTATEK_ERR_NULL, "eigvals, keep_mask, keep_idx required");
+  if (!aligned16(eigvals) || !aligned16(keep_mask) || !aligned16(keep_idx) || (info && !aligned16(info)))
+    return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
+  int n = 0;
+  rotatek_status s = launched(rk::launch_select_only(units, head_dim, rank, eigvals, keep_mask,
+                                                     keep_idx, info, reinterpret_cast<cudaStream_t>(stream)), &n);
+  if (s) return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
+}  // extern "C"

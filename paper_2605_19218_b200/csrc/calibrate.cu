@@ -1,0 +1,568 @@
+// calibrate.cu -- Alg. 1 (alg:rotatek-prefill) steps 1-5 on sm_100a:
+//   sigma -> centered covariance (Alg.1 l.1-3) -> Hadamard
+//   reweighting -> batched parallel Jacobi eigensolver (the "eigh" arm,
+//   P:653) -> top-r select + compaction + delta_mu.
+#include <cfloat>
+#include <cstdio>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace rk {
+
+// ============================================================== step 1: sigma
+// sigma[u][j] = sqrt(sum_{g,w} Qw[u][g][w][j]^2) in fp64 (reading Q4: pooled over
+// the G query heads of the unit).  sigma == 1 when !weight or W == 0.
+template <typename T>
+__global__ void sigma_kernel(int G, int W, int d, bool weight, const T* __restrict__ Qw,
+                             double* __restrict__ sigma) {
+  const int u = blockIdx.x;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double ss = 0.0;
+    if (weight && W > 0) {
+      const T* base = Qw + (size_t)u * G * W * d + j;
+      for (int row = 0; row < G * W; ++row) {
+        double x = Elem<T>::to_d(base[(size_t)row * d]);
+        ss = fma(x, x, ss);
+      }
+      sigma[(size_t)u * d + j] = sqrt(ss);
+    } else {
+      sigma[(size_t)u * d + j] = 1.0;
+    }
+  }
+}
+
+int launch_sigma(int U, int G, int W, int d, bool bf16, bool weight, const void* Qw,
+                 double* sigma, cudaStream_t st) {
+  int th = d < 128 ? 32 * ((d + 31) / 32) : 128;
+  if (bf16)
+    sigma_kernel<__nv_bfloat16><<<U, th, 0, st>>>(G, W, d, weight,
+                                                  (const __nv_bfloat16*)Qw, sigma);
+  else
+    sigma_kernel<float><<<U, th, 0, st>>>(G, W, d, weight, (const float*)Qw, sigma);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// ============================================================== step 2: covariance partials
+// Work item (tile, part, unit): the 64x64 upper tile (ti <= tj) of S = sum_n K_n K_n^T
+// over the token range of `part`, plus the column sums (diagonal tiles).  bf16 keys:
+// products are exact in fp32; fp32 accumulation over one 64-token chunk, then merged
+// into fp64 (precision scheme of SURVEY Appendix A, E-5/E-6).  fp32 keys: fp64 FMA.
+constexpr int kCovTile = 64;
+constexpr int kCovChunk = 64;
+
+template <typename T, typename Acc>
+__global__ void __launch_bounds__(256) cov_kernel(int N, int d, int parts, const T* __restrict__ K,
+                                                  double* __restrict__ covpart,
+                                                  double* __restrict__ colpart) {
+  __shared__ __align__(16) float Ki[kCovChunk][kCovTile];
+  __shared__ __align__(16) float Kj[kCovChunk][kCovTile];
+  const int u = blockIdx.z, p = blockIdx.y;
+  // unrank the upper tile index
+  const int nt = (d + kCovTile - 1) / kCovTile;
+  int ti = 0, rem = blockIdx.x;
+  while (rem >= nt - ti) { rem -= nt - ti; ++ti; }
+  const int tj = ti + rem;
+  const int ci0 = ti * kCovTile, cj0 = tj * kCovTile;
+  const bool diag = ti == tj;
+  const int n0 = (int)((long long)N * p / parts), n1 = (int)((long long)N * (p + 1) / parts);
+  const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+  const T* Ku = K + (size_t)u * N * d;
+
+  double accd[4][4];
+  Acc acc[4][4];
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) accd[a][b] = 0.0;
+  double cold = 0.0;
+
+  for (int c0 = n0; c0 < n1; c0 += kCovChunk) {
+    const int cn = min(kCovChunk, n1 - c0);
+    __syncthreads();
+    for (int e = tid; e < kCovChunk * kCovTile; e += 256) {
+      int t = e / kCovTile, c = e % kCovTile;
+      float vi = 0.f, vj = 0.f;
+      if (t < cn) {
+        if (ci0 + c < d) vi = Elem<T>::to_f(Ku[(size_t)(c0 + t) * d + ci0 + c]);
+        if (!diag && cj0 + c < d) vj = Elem<T>::to_f(Ku[(size_t)(c0 + t) * d + cj0 + c]);
+      }
+      Ki[t][c] = vi;
+      Kj[t][c] = diag ? vi : vj;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = Acc(0);
+    for (int t = 0; t < cn; ++t) {
+      float4 x = *reinterpret_cast<const float4*>(&Ki[t][4 * ty]);
+      float4 y = *reinterpret_cast<const float4*>(&Kj[t][4 * tx]);
+      Acc xa[4] = {Acc(x.x), Acc(x.y), Acc(x.z), Acc(x.w)};
+      Acc ya[4] = {Acc(y.x), Acc(y.y), Acc(y.z), Acc(y.w)};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(xa[a], ya[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) accd[a][b] += (double)acc[a][b];
+    if (diag && tid < kCovTile) {
+      Acc s = Acc(0);
+      for (int t = 0; t < cn; ++t) s += Acc(Ki[t][tid]);
+      cold += (double)s;
+    }
+  }
+  double* out = covpart + ((size_t)u * parts + p) * d * d;
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) {
+      int i = ci0 + 4 * ty + a, j = cj0 + 4 * tx + b;
+      if (i < d && j < d) out[(size_t)i * d + j] = accd[a][b];
+    }
+  if (diag && tid < kCovTile && ci0 + tid < d)
+    colpart[((size_t)u * parts + p) * d + ci0 + tid] = cold;
+}
+
+int cov_parts(int U, int N) {
+  int want = (2 * kNumSMs + U - 1) / U;  // >= ~2 CTAs per SM of work
+  int maxp = (N + 255) / 256;            // keep >= 256 tokens per part
+  int p = want < maxp ? want : maxp;
+  return p < 1 ? 1 : p;
+}
+
+int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws, cudaStream_t st) {
+  int nt = (d + kCovTile - 1) / kCovTile;
+  dim3 grid(nt * (nt + 1) / 2, ws.parts, U);
+  if (bf16)
+    cov_kernel<__nv_bfloat16, float><<<grid, 256, 0, st>>>(N, d, ws.parts,
+                                                          (const __nv_bfloat16*)K, ws.covpart,
+                                                          ws.colpart);
+  else
+    cov_kernel<float, double><<<grid, 256, 0, st>>>(N, d, ws.parts, (const float*)K, ws.covpart,
+                                                   ws.colpart);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// ============================================================== step 2b/3: finalize
+// mu = colsum / N ; C = S - N mu mu^T (fp64) ; C_q = (sigma sigma^T) (.) C.  Reads only the
+// upper tiles (a <= b), so C_q is exactly symmetric.
+__global__ void __launch_bounds__(256) finalize_kernel(int N, int d, int parts, bool center,
+                                                       const double* __restrict__ covpart,
+                                                       const double* __restrict__ colpart,
+                                                       const double* __restrict__ sigma,
+                                                       double* __restrict__ cq,
+                                                       double* __restrict__ mu_out) {
+  extern __shared__ double sh_mu[];  // [d] mu, [d] sigma
+  double* sh_sig = sh_mu + d;
+  const int u = blockIdx.x;
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    double s = 0.0;
+    for (int p = 0; p < parts; ++p) s += colpart[((size_t)u * parts + p) * d + j];
+    double m = center ? s / (double)N : 0.0;
+    sh_mu[j] = m;
+    mu_out[(size_t)u * d + j] = m;
+    sh_sig[j] = sigma[(size_t)u * d + j];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+    int i = e / d, j = e % d;
+    int a = min(i, j), b = max(i, j);
+    double s = 0.0;
+    for (int p = 0; p < parts; ++p) s += covpart[((size_t)u * parts + p) * d * d + (size_t)a * d + b];
+    double c = s - (double)N * sh_mu[a] * sh_mu[b];
+    cq[(size_t)u * d * d + e] = sh_sig[a] * sh_sig[b] * c;
+  }
+}
+
+int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st) {
+  finalize_kernel<<<U, 256, 2 * d * sizeof(double), st>>>(N, d, ws.parts, center, ws.covpart,
+                                                          ws.colpart, ws.sigma, ws.cq, ws.mu);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// ============================================================== step 4: batched Jacobi
+// One CTA per unit.  Parallel (round-robin / "circle method") ordering: each sweep is
+// d-1 rounds of d/2 disjoint pairs (p, q).  A round computes the d/2 symmetric Schur
+// rotations (c, s, t) from a_pp, a_qq, a_pq, then applies all of them at once:
+// every 2x2 block (pair a x pair b) of A becomes J_a^T X J_b and every row of V gets
+// V[x, (p_b, q_b)] <- V[x, (p_b, q_b)] J_b.  A is held in packed upper-triangle form
+// in shared memory, V dense (row stride d+1).  Convergence: off(A) <= tol ||A||_F,
+// checked once per sweep.  Input is pre-scaled by an exact power of two to ||A||_F ~ 1.
+__device__ __forceinline__ int pidx(int i, int j, int d) {  // i <= j
+  return i * d - (i * (i - 1)) / 2 + (j - i);
+}
+
+template <typename T>
+__device__ __forceinline__ T rsqrt_t(T x);
+template <>
+__device__ __forceinline__ float rsqrt_t<float>(float x) { return 1.0f / sqrtf(x); }
+template <>
+__device__ __forceinline__ double rsqrt_t<double>(double x) { return 1.0 / sqrt(x); }
+
+template <typename T>
+__device__ T block_sum(T v, T* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  T s = T(0);
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+constexpr int kJacobiThreads = 256;
+
+size_t jacobi_smem_bytes(int d, bool fp64) {
+  size_t ts = fp64 ? 8 : 4;
+  int h = d / 2;
+  size_t np = (size_t)d * (d + 1) / 2;
+  size_t nblk = (size_t)h * (h + 1) / 2;
+  size_t b = (np + (size_t)d * (d + 1) + 3 * h + 32) * ts;
+  b += (2 * h + nblk) * sizeof(uint16_t);
+  return (b + 15) & ~(size_t)15;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(int d, const double* __restrict__ cq,
+                                                                float* __restrict__ lam_out,
+                                                                T* __restrict__ vecs,
+                                                                int32_t* __restrict__ jinfo, T tol,
+                                                                int max_sweeps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int u = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
+  const int h = d / 2, ldv = d + 1;
+  const int np = d * (d + 1) / 2;
+  const int nblk = h * (h + 1) / 2;
+  T* A = reinterpret_cast<T*>(smem_raw);
+  T* V = A + np;
+  T* cs = V + d * ldv;
+  T* sn = cs + h;
+  T* tt = sn + h;
+  T* red = tt + h;
+  uint16_t* Pp = reinterpret_cast<uint16_t*>(red + 32);
+  uint16_t* Qp = Pp + h;
+  uint16_t* blk = Qp + h;
+  __shared__ double s_red[32];
+  __shared__ int s_bad;
+
+  const double* C = cq + (size_t)u * d * d;
+  // ---- norm, finiteness, exact power-of-two scaling
+  double f2 = 0.0;
+  int bad = 0;
+  for (int e = tid; e < d * d; e += nth) {
+    double x = C[e];
+    if (!isfinite(x)) bad = 1;
+    f2 = fma(x, x, f2);
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  if (bad) s_bad = 1;
+  f2 = block_sum<double>(f2, s_red);
+  __syncthreads();
+  if (s_bad) {
+    for (int e = tid; e < d * d; e += nth) vecs[(size_t)u * d * d + e] = T(0);
+    for (int j = tid; j < d; j += nth) lam_out[(size_t)u * d + j] = CUDART_NAN_F;
+    if (tid == 0) jinfo[u] = -1;
+    return;
+  }
+  int ex = 0;
+  if (f2 > 0.0) frexp(sqrt(f2), &ex);
+  const double scale = ldexp(1.0, -ex), unscale = ldexp(1.0, ex);
+  const int wid = tid >> 5, lane = tid & 31, nwarp = nth >> 5;
+  for (int i = wid; i < d; i += nwarp)
+    for (int j = i + lane; j < d; j += 32) A[pidx(i, j, d)] = T(C[(size_t)i * d + j] * scale);
+  for (int e = tid; e < d * ldv; e += nth) {
+    int x = e / ldv, c = e % ldv;
+    V[e] = (x == c) ? T(1) : T(0);
+  }
+  for (int e = tid; e < nblk; e += nth) {
+    int a = 0, rem = e;
+    while (rem >= h - a) { rem -= h - a; ++a; }
+    blk[e] = (uint16_t)(a | ((a + rem) << 8));
+  }
+  __syncthreads();
+  T fro2 = T(0);
+  for (int i = wid; i < d; i += nwarp)
+    for (int j = i + lane; j < d; j += 32) {
+      const T a = A[pidx(i, j, d)];
+      fro2 += (j == i ? T(1) : T(2)) * a * a;
+    }
+  fro2 = block_sum<T>(fro2, red);
+
+  int sweep = 0, converged = 0;
+  for (;; ++sweep) {
+    T off2 = T(0);
+    for (int i = wid; i < d; i += nwarp)
+      for (int j = i + 1 + lane; j < d; j += 32) {
+        const T a = A[pidx(i, j, d)];
+        off2 += T(2) * a * a;
+      }
+    off2 = block_sum<T>(off2, red);
+    if (off2 <= tol * tol * fro2) { converged = 1; break; }
+    if (sweep >= max_sweeps) break;
+    for (int k = 0; k < d - 1; ++k) {
+      if (tid < h) {
+        int p, q;
+        if (tid == 0) { p = k; q = d - 1; }
+        else {
+          p = (k + tid) % (d - 1);
+          q = (k - tid + (d - 1)) % (d - 1);
+        }
+        if (p > q) { int t = p; p = q; q = t; }
+        T apq = A[pidx(p, q, d)];
+        T c = T(1), s = T(0), t = T(0);
+        if (apq != T(0)) {
+          T app = A[pidx(p, p, d)], aqq = A[pidx(q, q, d)];
+          T tau = (aqq - app) / (T(2) * apq);
+          T at = tau >= T(0) ? tau : -tau;
+          t = (tau >= T(0) ? T(1) : T(-1)) / (at + sqrt(T(1) + tau * tau));
+          c = rsqrt_t<T>(T(1) + t * t);
+          s = t * c;
+        }
+        cs[tid] = c; sn[tid] = s; tt[tid] = t;
+        Pp[tid] = (uint16_t)p; Qp[tid] = (uint16_t)q;
+      }
+      __syncthreads();
+      for (int e = tid; e < nblk; e += nth) {
+        const int a = blk[e] & 0xFF, b = blk[e] >> 8;
+        const int pa = Pp[a], qa = Qp[a];
+        if (a == b) {
+          const int ipp = pidx(pa, pa, d), iqq = pidx(qa, qa, d), ipq = pidx(pa, qa, d);
+          const T apq = A[ipq], t = tt[a];
+          A[ipp] = A[ipp] - t * apq;
+          A[iqq] = A[iqq] + t * apq;
+          A[ipq] = T(0);
+        } else {
+          const int pb = Pp[b], qb = Qp[b];
+          const T ca = cs[a], sa = sn[a], cb = cs[b], sb = sn[b];
+          const int i00 = pidx(min(pa, pb), max(pa, pb), d);
+          const int i01 = pidx(min(pa, qb), max(pa, qb), d);
+          const int i10 = pidx(min(qa, pb), max(qa, pb), d);
+          const int i11 = pidx(min(qa, qb), max(qa, qb), d);
+          const T x00 = A[i00], x01 = A[i01], x10 = A[i10], x11 = A[i11];
+          // L = J_a^T X  (rows p_a, q_a)
+          const T l00 = ca * x00 - sa * x10, l01 = ca * x01 - sa * x11;
+          const T l10 = sa * x00 + ca * x10, l11 = sa * x01 + ca * x11;
+          // Y = L J_b  (cols p_b, q_b)
+          A[i00] = cb * l00 - sb * l01;
+          A[i01] = sb * l00 + cb * l01;
+          A[i10] = cb * l10 - sb * l11;
+          A[i11] = sb * l10 + cb * l11;
+        }
+      }
+      for (int e = tid; e < d * h; e += nth) {
+        const int x = e % d, b = e / d;
+        const int pb = Pp[b], qb = Qp[b];
+        const T c = cs[b], s = sn[b];
+        const T vp = V[x * ldv + pb], vq = V[x * ldv + qb];
+        V[x * ldv + pb] = c * vp - s * vq;
+        V[x * ldv + qb] = s * vp + c * vq;
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = tid; j < d; j += nth) lam_out[(size_t)u * d + j] = (float)((double)A[pidx(j, j, d)] * unscale);
+  for (int e = tid; e < d * d; e += nth) vecs[(size_t)u * d * d + e] = V[(e / d) * ldv + (e % d)];
+  if (tid == 0) jinfo[u] = converged ? 0 : (sweep > 0 ? sweep : 1);
+}
+
+int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st) {
+  size_t sm = jacobi_smem_bytes(d, fp64);
+  if (fp64) {
+    cudaFuncSetAttribute(jacobi_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    jacobi_kernel<double><<<U, kJacobiThreads, sm, st>>>(d, ws.cq, ws.lam, (double*)ws.vecs,
+                                                         ws.jinfo, 1e-13, 40);
+  } else {
+    cudaFuncSetAttribute(jacobi_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    jacobi_kernel<float><<<U, kJacobiThreads, sm, st>>>(d, ws.cq, ws.lam, (float*)ws.vecs,
+                                                        ws.jinfo, 1e-6f, 30);
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// ============================================================== step 5: top-r select
+// Warp-level, sort-free and bit-exact: rank_i = #{j : l_j > l_i or (l_j == l_i and j < i)},
+// keep iff rank_i < r; __ballot_sync builds the d-bit head mask; a popc prefix gives the
+// compaction slot, so kept channels are listed in ascending index.  NaN -> returns false.
+constexpr int kMaxSlots = 8;  // d <= 256
+
+__device__ bool warp_select(const float* __restrict__ lam, int d, int r, uint32_t* mask_sm,
+                            int* kidx_sm) {
+  const int lane = threadIdx.x & 31;
+  float v[kMaxSlots];
+  int rank[kMaxSlots];
+  bool has_nan = false;
+#pragma unroll
+  for (int s = 0; s < kMaxSlots; ++s) {
+    int i = 32 * s + lane;
+    v[s] = i < d ? lam[i] : 0.f;
+    rank[s] = 0;
+    if (i < d && isnan(v[s])) has_nan = true;
+  }
+  if (__any_sync(0xffffffffu, has_nan)) return false;
+#pragma unroll
+  for (int s = 0; s < kMaxSlots; ++s) {
+    if (32 * s >= d) break;
+    for (int src = 0; src < 32; ++src) {
+      const int j = 32 * s + src;
+      if (j >= d) break;
+      const float lj = __shfl_sync(0xffffffffu, v[s], src);
+#pragma unroll
+      for (int k = 0; k < kMaxSlots; ++k) {
+        const int i = 32 * k + lane;
+        rank[k] += (lj > v[k] || (lj == v[k] && j < i)) ? 1 : 0;
+      }
+    }
+  }
+  int before = 0;
+#pragma unroll
+  for (int s = 0; s < kMaxSlots; ++s) {
+    if (32 * s >= d) break;
+    const int i = 32 * s + lane;
+    const bool keep = i < d && rank[s] < r;
+    const uint32_t m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) mask_sm[s] = m;
+    if (keep) kidx_sm[before + __popc(m & ((1u << lane) - 1u))] = i;
+    before += __popc(m);
+  }
+  __syncwarp();
+  return true;
+}
+
+template <typename TV>
+__global__ void __launch_bounds__(128) select_gather_kernel(
+    int d, int r, bool bf16x2, bool center, const float* __restrict__ lam,
+    const TV* __restrict__ vecs, const double* __restrict__ mu, const int32_t* __restrict__ jinfo,
+    float* __restrict__ R, float* __restrict__ dmu, float* __restrict__ eigvals,
+    uint32_t* __restrict__ mask, int32_t* __restrict__ idx, float* __restrict__ R_full,
+    int32_t* __restrict__ info) {
+  extern __shared__ __align__(16) unsigned char sm[];
+  float* Rs = reinterpret_cast<float*>(sm);                 // [d][r]
+  double* proj = reinterpret_cast<double*>(Rs + d * r + (d * r & 1));  // [r]
+  double* mus = proj + r;                                   // [d]
+  __shared__ uint32_t mask_sm[kMaxSlots];
+  __shared__ int kidx_sm[256];
+  __shared__ int s_ok;
+  const int u = blockIdx.x, tid = threadIdx.x;
+  const int words = (d + 31) / 32;
+  const float* lu = lam + (size_t)u * d;
+  if (tid < 32) {
+    bool ok = jinfo[u] != -1 && warp_select(lu, d, r, mask_sm, kidx_sm);
+    if (tid == 0) s_ok = ok;
+  }
+  __syncthreads();
+  if (eigvals && eigvals != lam)
+    for (int j = tid; j < d; j += blockDim.x) eigvals[(size_t)u * d + j] = lu[j];
+  if (!s_ok) {
+    for (int e = tid; e < d * r; e += blockDim.x) R[(size_t)u * d * r + e] = 0.f;
+    for (int j = tid; j < d; j += blockDim.x) dmu[(size_t)u * d + j] = 0.f;
+    if (mask) for (int w = tid; w < words; w += blockDim.x) mask[(size_t)u * words + w] = 0u;
+    if (idx) for (int k = tid; k < r; k += blockDim.x) idx[(size_t)u * r + k] = -1;
+    if (R_full) for (int e = tid; e < d * d; e += blockDim.x) R_full[(size_t)u * d * d + e] = 0.f;
+    if (info && tid == 0) info[u] = -1;
+    return;
+  }
+  if (mask) for (int w = tid; w < words; w += blockDim.x) mask[(size_t)u * words + w] = mask_sm[w];
+  if (idx) for (int k = tid; k < r; k += blockDim.x) idx[(size_t)u * r + k] = kidx_sm[k];
+  const TV* Vu = vecs + (size_t)u * d * d;
+  for (int e = tid; e < d * r; e += blockDim.x) {
+    const int x = e / r, k = e % r;
+    float v = (float)Vu[(size_t)x * d + kidx_sm[k]];
+    (void)bf16x2;  // R is stored as plain fp32 (RNE of the solver value)
+    Rs[e] = v;
+    R[(size_t)u * d * r + e] = v;
+  }
+  if (R_full)
+    for (int e = tid; e < d * d; e += blockDim.x) R_full[(size_t)u * d * d + e] = (float)Vu[e];
+  for (int j = tid; j < d; j += blockDim.x) mus[j] = center ? mu[(size_t)u * d + j] : 0.0;
+  __syncthreads();
+  // delta_mu = mu - R_r (R_r^T mu) in fp64 from the STORED R_r
+  for (int k = tid; k < r; k += blockDim.x) {
+    double s = 0.0;
+    for (int x = 0; x < d; ++x) s = fma((double)Rs[x * r + k], mus[x], s);
+    proj[k] = s;
+  }
+  __syncthreads();
+  for (int x = tid; x < d; x += blockDim.x) {
+    double s = 0.0;
+    for (int k = 0; k < r; ++k) s = fma((double)Rs[x * r + k], proj[k], s);
+    dmu[(size_t)u * d + x] = (float)(mus[x] - s);
+  }
+  if (info && tid == 0) info[u] = jinfo[u];
+}
+
+int launch_select_gather(int U, int d, int r, bool fp64_vecs, bool bf16x2, bool center,
+                         const CalibWs& ws, float* R, float* dmu, float* eigvals, uint32_t* mask,
+                         int32_t* idx, float* R_full, int32_t* info, cudaStream_t st) {
+  size_t sm = (size_t)d * r * 4 + 8 + (size_t)(r + d) * 8 + 16;
+  if (fp64_vecs) {
+    cudaFuncSetAttribute(select_gather_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    select_gather_kernel<double><<<U, 128, sm, st>>>(d, r, bf16x2, center, ws.lam,
+                                                     (const double*)ws.vecs, ws.mu, ws.jinfo, R,
+                                                     dmu, eigvals, mask, idx, R_full, info);
+  } else {
+    cudaFuncSetAttribute(select_gather_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    select_gather_kernel<float><<<U, 128, sm, st>>>(d, r, bf16x2, center, ws.lam,
+                                                    (const float*)ws.vecs, ws.mu, ws.jinfo, R, dmu,
+                                                    eigvals, mask, idx, R_full, info);
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// standalone select (rotatek_select_topr): one warp per unit, 4 units per CTA
+__global__ void __launch_bounds__(128) select_only_kernel(int U, int d, int r,
+                                                          const float* __restrict__ lam,
+                                                          uint32_t* __restrict__ mask,
+                                                          int32_t* __restrict__ idx,
+                                                          int32_t* __restrict__ info) {
+  __shared__ uint32_t mask_sm[4][kMaxSlots];
+  __shared__ int kidx_sm[4][256];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x * 4 + w;
+  if (u >= U) return;
+  const int words = (d + 31) / 32;
+  bool ok = warp_select(lam + (size_t)u * d, d, r, mask_sm[w], kidx_sm[w]);
+  for (int k = lane; k < words; k += 32) mask[(size_t)u * words + k] = ok ? mask_sm[w][k] : 0u;
+  for (int k = lane; k < r; k += 32) idx[(size_t)u * r + k] = ok ? kidx_sm[w][k] : -1;
+  if (info && lane == 0) info[u] = ok ? 0 : -1;
+}
+
+int launch_select_only(int U, int d, int r, const float* lam, uint32_t* mask, int32_t* idx,
+                       int32_t* info, cudaStream_t st) {
+  select_only_kernel<<<(U + 3) / 4, 128, 0, st>>>(U, d, r, lam, mask, idx, info);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// ============================================================== workspace layout
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+size_t calib_ws_layout(int U, int d, int N, bool fp64_eig, void* base, CalibWs* ws) {
+  const int P = cov_parts(U, N);
+  size_t off = 0;
+  char* b = static_cast<char*>(base);
+  auto take = [&](size_t bytes) -> void* {
+    void* p = b ? b + off : nullptr;
+    off += al256(bytes);
+    return p;
+  };
+  CalibWs w;
+  w.parts = P;
+  w.sigma = (double*)take((size_t)U * d * 8);
+  w.covpart = (double*)take((size_t)U * P * d * d * 8);
+  w.colpart = (double*)take((size_t)U * P * d * 8);
+  w.cq = (double*)take((size_t)U * d * d * 8);
+  w.mu = (double*)take((size_t)U * d * 8);
+  w.lam = (float*)take((size_t)U * d * 4);
+  w.vecs = take((size_t)U * d * d * (fp64_eig ? 8 : 4));
+  w.jinfo = (int32_t*)take((size_t)U * 4);
+  if (ws) *ws = w;
+  return off;
+}
+
+}  // namespace rk

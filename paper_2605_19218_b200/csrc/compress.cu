@@ -1,0 +1,64 @@
+// compress.cu -- Alg. 1 line 14: K~ = K R_r, stored in place of K,
+// rounded (RNE) to the cache dtype.  R_r is the stored calibrate output (bf16 path: every
+// value is exactly bf16_hi + bf16_lo), used identically by decode for q~ (reading E-11).
+//
+// v1: CUDA-core fp32 FMA.  One CTA per (64-token tile, unit); R_r [d, r] and the K tile
+// [64, d] are staged in shared memory as fp32; each warp owns 8 tokens, each lane a
+// strided set of output channels.
+#include "common.cuh"
+#include "internal.h"
+
+namespace rk {
+
+constexpr int kCmpTok = 64;
+
+template <typename T>
+__global__ void __launch_bounds__(256) compress_kernel(int N, int d, int r, const T* __restrict__ K,
+                                                       const float* __restrict__ R,
+                                                       T* __restrict__ Kc) {
+  extern __shared__ __align__(16) float csm[];
+  float* Rs = csm;               // [d][r]
+  float* Ks = csm + d * r;       // [kCmpTok][d]
+  const int u = blockIdx.y, t0 = blockIdx.x * kCmpTok;
+  const int tn = min(kCmpTok, N - t0);
+  const int tid = threadIdx.x;
+  const float* Ru = R + (size_t)u * d * r;
+  for (int e = tid; e < d * r; e += blockDim.x) Rs[e] = Ru[e];
+  const T* Ku = K + ((size_t)u * N + t0) * d;
+  for (int e = tid; e < tn * d; e += blockDim.x) Ks[e] = Elem<T>::to_f(Ku[e]);
+  __syncthreads();
+  const int w = tid >> 5, lane = tid & 31;
+  T* out = Kc + ((size_t)u * N + t0) * r;
+  for (int k = lane; k < r; k += 32) {
+    float acc[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+    for (int i = 0; i < d; ++i) {
+      const float rv = Rs[i * r + k];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = fmaf(Ks[(w * 8 + j) * d + i], rv, acc[j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int t = w * 8 + j;
+      if (t < tn) out[(size_t)t * r + k] = Elem<T>::from_f(acc[j]);
+    }
+  }
+}
+
+int launch_compress(int U, int N, int d, int r, bool bf16, const void* K, const float* R,
+                    void* Kc, cudaStream_t st) {
+  dim3 grid((N + kCmpTok - 1) / kCmpTok, U);
+  size_t sm = ((size_t)d * r + (size_t)kCmpTok * d) * sizeof(float);
+  if (bf16) {
+    cudaFuncSetAttribute(compress_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    compress_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(N, d, r, (const __nv_bfloat16*)K, R,
+                                                         (__nv_bfloat16*)Kc);
+  } else {
+    cudaFuncSetAttribute(compress_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    compress_kernel<float><<<grid, 256, sm, st>>>(N, d, r, (const float*)K, R, (float*)Kc);
+  }
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace rk

@@ -1,0 +1,67 @@
+// internal.h -- host-side launchers behind the C ABI (not exported).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace rk {
+
+constexpr int kNumSMs = 148;
+
+struct CalibWs {
+  double* sigma;     // [U, d]
+  double* covpart;   // [U, P, d, d]   upper tiles valid
+  double* colpart;   // [U, P, d]
+  double* cq;        // [U, d, d]
+  double* mu;        // [U, d]
+  float* lam;        // [U, d]
+  void* vecs;        // [U, d, d] float or double
+  int32_t* jinfo;    // [U]
+  int parts;         // P token partitions per unit
+};
+
+struct DecodeWs {
+  uint32_t* counters;  // [U] zero on entry, left zero
+  float* partials;     // [U, G, S, d + 2]
+  int max_splits;
+};
+
+int cov_parts(int U, int N);
+int decode_max_splits(int U, int N, int M);
+size_t calib_ws_layout(int U, int d, int N, bool fp64_eig, void* base, CalibWs* ws);
+size_t decode_ws_layout(int U, int G, int d, int N, int M, void* base, DecodeWs* ws);
+
+// each returns the number of launches enqueued (>= 0) or -1 on launch error
+int launch_sigma(int U, int G, int W, int d, bool bf16, bool weight, const void* Qw,
+                 double* sigma, cudaStream_t st);
+int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws, cudaStream_t st);
+int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st);
+int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st);
+int launch_select_gather(int U, int d, int r, bool fp64_vecs, bool bf16x2, bool center,
+                         const CalibWs& ws, float* R, float* dmu, float* eigvals,
+                         uint32_t* mask, int32_t* idx, float* R_full, int32_t* info,
+                         cudaStream_t st);
+int launch_select_only(int U, int d, int r, const float* lam, uint32_t* mask, int32_t* idx,
+                       int32_t* info, cudaStream_t st);
+int launch_compress(int U, int N, int d, int r, bool bf16, const void* K, const float* R,
+                    void* Kc, cudaStream_t st);
+
+struct DecodeArgs {
+  int U, G, d, r, N, M;
+  bool bf16;
+  const void* q;
+  const void* Kc;
+  const void* V;
+  const float* R;
+  const float* dmu;
+  const void* Kt;
+  const void* Vt;
+  float scale;
+  float* out;
+};
+// kernel: 0 auto, 1 generic, 2 fast.  Returns launches, -1 launch error, -2 unsupported.
+int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kernel,
+                  cudaStream_t st);
+
+}  // namespace rk

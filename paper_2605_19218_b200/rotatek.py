@@ -1,0 +1,222 @@
+"""Thin Python binding of librotatek.so (include/rotatek.h).
+
+Argument marshalling only: shapes are read from the torch tensors, outputs and
+zero-filled workspaces are allocated with torch (device memory is plumbing),
+and every step of the hot path runs in the library's sm_100a kernels.  There
+is no CPU or PyTorch fallback: if the library is missing or a call fails, a
+RuntimeError is raised.
+
+Names follow the paper: K (visual keys), Qw (query window Q_W), R (R_r, the kept
+eigenvectors), dmu (delta_mu), K_comp (K~), K_text/V_text (prompt+text K_pt, V).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librotatek.so")
+
+OK, ERR_NULL, ERR_DIMS, ERR_ALIGN, ERR_WORKSPACE, ERR_UNSUPPORTED, ERR_CUDA = range(7)
+BF16, F32 = 0, 1
+CENTER, QUERY_WEIGHT, EIG_FP32 = 1, 2, 4
+DEFAULT_FLAGS = CENTER | QUERY_WEIGHT
+OP_CALIBRATE, OP_DECODE = 0, 1
+KERNEL_AUTO, KERNEL_GENERIC, KERNEL_FAST = 0, 1, 2
+
+
+class Dims(ctypes.Structure):
+    _fields_ = [("units", ctypes.c_int32), ("group", ctypes.c_int32),
+                ("head_dim", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("n_vis", ctypes.c_int32), ("n_text", ctypes.c_int32),
+                ("q_window", ctypes.c_int32), ("dtype", ctypes.c_int32)]
+
+
+class RotateKError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        super().__init__(what)
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def lib():
+    """Load librotatek.so (fails loudly if it has not been built)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(f"{LIB_PATH} is missing: build it with `make` or "
+                                   "`python -c 'import __graft_entry__ as g; g.build()'`")
+            L = ctypes.CDLL(LIB_PATH)
+            vp, sz, u32, i32, f = (ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint32,
+                                   ctypes.c_int32, ctypes.c_float)
+            dp = ctypes.POINTER(Dims)
+            L.rotatek_workspace_bytes.argtypes = [dp, ctypes.c_int]
+            L.rotatek_workspace_bytes.restype = sz
+            L.rotatek_calibrate.argtypes = [dp, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+            L.rotatek_compress_kv.argtypes = [dp, vp, vp, vp, vp]
+            L.rotatek_decode_attn.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz, vp]
+            L.rotatek_decode_attn_ex.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz,
+                                                 i32, i32, vp]
+            L.rotatek_select_topr.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp]
+            for fn in ("rotatek_calibrate", "rotatek_compress_kv", "rotatek_decode_attn",
+                       "rotatek_decode_attn_ex", "rotatek_select_topr"):
+                getattr(L, fn).restype = ctypes.c_int
+            L.rotatek_status_string.argtypes = [ctypes.c_int]
+            L.rotatek_status_string.restype = ctypes.c_char_p
+            L.rotatek_last_error.restype = ctypes.c_char_p
+            L.rotatek_abi_version.restype = ctypes.c_int
+            L.rotatek_last_launch_count.restype = ctypes.c_int
+            _lib = L
+    return _lib
+
+
+def _check(status: int):
+    if status != OK:
+        L = lib()
+        raise RotateKError(status, f"{L.rotatek_status_string(status).decode()}: "
+                                   f"{L.rotatek_last_error().decode()}")
+
+
+def last_launch_count() -> int:
+    return lib().rotatek_last_launch_count()
+
+
+def _dtype_code(t: torch.Tensor) -> int:
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return F32
+    raise TypeError(f"unsupported dtype {t.dtype}; use bfloat16 or float32")
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if not t.is_cuda:
+        raise ValueError("librotatek takes device tensors")
+    if not t.is_contiguous():
+        raise ValueError("tensors must be contiguous")
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def make_dims(units, group, head_dim, rank, n_vis, n_text=0, q_window=0, dtype=BF16) -> Dims:
+    return Dims(int(units), int(group), int(head_dim), int(rank), int(n_vis), int(n_text),
+                int(q_window), int(dtype))
+
+
+def workspace_bytes(dims: Dims, op: int) -> int:
+    return int(lib().rotatek_workspace_bytes(ctypes.byref(dims), op))
+
+
+_ws_cache: dict = {}
+
+
+def workspace(dims: Dims, op: int, device) -> torch.Tensor:
+    """Zero-filled workspace (the ABI requires zero on first use; calls leave it zeroed).
+    Cached per (device, op, size) for the current thread's stream."""
+    n = workspace_bytes(dims, op)
+    if n == 0:
+        _check(ERR_DIMS)
+    key = (str(device), op, n, torch.cuda.current_stream(device).cuda_stream)
+    t = _ws_cache.get(key)
+    if t is None:
+        t = torch.zeros(n, dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+# --------------------------------------------------------------------------- calibrate
+def calibrate(K: torch.Tensor, Qw: torch.Tensor | None, rank: int, flags: int = DEFAULT_FLAGS,
+              *, want_full: bool = False, ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Alg. 1 steps 1-5 (+ select, delta_mu).  K [U, N, d]; Qw [U, G, W, d] or None.
+
+    Returns dict(R [U,d,r] f32, dmu [U,d] f32, eigvals [U,d] f32, mask [U,ceil(d/32)] i32
+    (uint32 bit pattern), idx [U,r] i32, info [U] i32, R_full [U,d,d] f32 if want_full)."""
+    U, N, d = K.shape
+    if Qw is None:
+        G, W = 1, 0
+    else:
+        assert Qw.dim() == 4 and Qw.shape[0] == U and Qw.shape[3] == d and Qw.dtype == K.dtype
+        G, W = Qw.shape[1], Qw.shape[2]
+    dims = make_dims(U, G, d, rank, N, 0, W, _dtype_code(K))
+    dev = K.device
+    out = dict(
+        R=torch.empty((U, d, rank), dtype=torch.float32, device=dev),
+        dmu=torch.empty((U, d), dtype=torch.float32, device=dev),
+        eigvals=torch.empty((U, d), dtype=torch.float32, device=dev),
+        mask=torch.empty((U, (d + 31) // 32), dtype=torch.int32, device=dev),
+        idx=torch.empty((U, rank), dtype=torch.int32, device=dev),
+        info=torch.empty((U,), dtype=torch.int32, device=dev),
+    )
+    out["R_full"] = torch.empty((U, d, d), dtype=torch.float32, device=dev) if want_full else None
+    if ws is None:
+        ws = workspace(dims, OP_CALIBRATE, dev)
+    _check(lib().rotatek_calibrate(ctypes.byref(dims), flags, _ptr(K),
+                                   _ptr(Qw) if W > 0 else None, _ptr(out["R"]), _ptr(out["dmu"]),
+                                   _ptr(out["eigvals"]), _ptr(out["mask"]), _ptr(out["idx"]),
+                                   _ptr(out["R_full"]), _ptr(out["info"]), _ptr(ws), ws.numel(),
+                                   _stream(stream)))
+    return out
+
+
+# --------------------------------------------------------------------------- compress
+def compress_kv(K: torch.Tensor, R: torch.Tensor, out: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+    """Alg. 1 line 14: K~ = RNE(K R_r).  K [U, N, d], R [U, d, r] f32 -> [U, N, r] K.dtype."""
+    U, N, d = K.shape
+    r = R.shape[2]
+    assert R.shape == (U, d, r) and R.dtype == torch.float32
+    if out is None:
+        out = torch.empty((U, N, r), dtype=K.dtype, device=K.device)
+    dims = make_dims(U, 1, d, r, N, 0, 0, _dtype_code(K))
+    _check(lib().rotatek_compress_kv(ctypes.byref(dims), _ptr(K), _ptr(R), _ptr(out),
+                                     _stream(stream)))
+    return out
+
+
+# --------------------------------------------------------------------------- decode
+def decode_attn(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, R: torch.Tensor,
+                dmu: torch.Tensor | None, K_text: torch.Tensor | None = None,
+                V_text: torch.Tensor | None = None, scale: float = 0.0,
+                out: torch.Tensor | None = None, *, splits: int = 0, kernel: int = KERNEL_AUTO,
+                ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Alg. 2 for all query heads: q [U, G, d], K_comp [U, N, r], V [U, N, d], R [U, d, r],
+    dmu [U, d] | None, K_text/V_text [U, M, d] | None -> out [U, G, d] f32."""
+    U, G, d = q.shape
+    N, r = K_comp.shape[1], K_comp.shape[2]
+    M = 0 if K_text is None else K_text.shape[1]
+    assert V.shape == (U, N, d) and R.shape == (U, d, r)
+    dims = make_dims(U, G, d, r, N, M, 0, _dtype_code(K_comp))
+    if out is None:
+        out = torch.empty((U, G, d), dtype=torch.float32, device=q.device)
+    if ws is None:
+        ws = workspace(dims, OP_DECODE, q.device)
+    _check(lib().rotatek_decode_attn_ex(ctypes.byref(dims), _ptr(q), _ptr(K_comp), _ptr(V),
+                                        _ptr(R), _ptr(dmu), _ptr(K_text) if M else None,
+                                        _ptr(V_text) if M else None, float(scale), _ptr(out),
+                                        _ptr(ws), ws.numel(), int(splits), int(kernel),
+                                        _stream(stream)))
+    return out
+
+
+def select_topr(eigvals: torch.Tensor, rank: int, stream=None):
+    """Top-r select on given eigenvalues [U, d] f32 -> (mask [U, ceil(d/32)], idx [U, r], info [U])."""
+    U, d = eigvals.shape
+    mask = torch.empty((U, (d + 31) // 32), dtype=torch.int32, device=eigvals.device)
+    idx = torch.empty((U, rank), dtype=torch.int32, device=eigvals.device)
+    info = torch.empty((U,), dtype=torch.int32, device=eigvals.device)
+    _check(lib().rotatek_select_topr(U, d, rank, _ptr(eigvals), _ptr(mask), _ptr(idx), _ptr(info),
+                                     _stream(stream)))
+    return mask, idx, info

@@ -1,0 +1,328 @@
+"""GPU parity: librotatek (sm_100a) against the fp64 oracle, through the C ABI.
+
+Gates:
+  G-dec  decode on the exact bytes the GPU holds      <= 2e-3 (bf16) / 1e-5 (fp32)  (Q23 metric)
+  G-sel  select masks / indices                        bit-exact
+  G-cal  calibration (planted-gap data)                projector distance, orthonormality, ...
+  G-cmp  compress                                       K~ vs RNE(K R) on the GPU's R
+  G-e2e  calibrate + compress + decode vs oracle 1-8   <= 2e-3 (bf16) / 1e-5 (fp32)
+"""
+import numpy as np
+import pytest
+
+from helpers import max_rel_err, mask_bits_u32, to_np64, to_torch
+from oracle import oracle as orc
+from workload import CONFIGS, make_workload
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"bf16": 2e-3, "f32": 1e-5}
+
+
+@pytest.fixture(scope="module")
+def rk():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_2605_19218_b200 as rk
+    rk.lib()
+    return rk
+
+
+def _torch_dtype(dtype):
+    import torch
+    return torch.bfloat16 if dtype == "bf16" else torch.float32
+
+
+def _as_dev(x_f64, dtype):
+    """fp64 numpy holding values exactly representable in dtype -> device tensor."""
+    import torch
+    return torch.from_numpy(np.asarray(x_f64, dtype=np.float32)).to(_torch_dtype(dtype)).cuda()
+
+
+def _cache_from_oracle(cfg, w, dtype):
+    """Oracle calibrate + quantised K~ (the bytes the decode kernel will read)."""
+    cal = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
+    R32 = cal["R"].astype(np.float32).astype(np.float64)
+    Kt = orc.quantize(orc.compress(w["K"].f64(), R32), dtype)
+    dmu32 = cal["dmu"].astype(np.float32).astype(np.float64)
+    return R32, dmu32, Kt
+
+
+SMALL = {
+    "toy": CONFIGS["toy"],
+    "llava_small": CONFIGS["llava_b1"].with_(h_kv=3, n_vis=333, n_text=37),
+    "qwen_small_r32": CONFIGS["qwen_b1_r32"].with_(h_kv=2, n_vis=517, n_text=21),
+    "qwen_small_r64": CONFIGS["qwen_b1_r32"].with_(h_kv=2, rank=64, n_vis=300, n_text=0),
+    "r16": CONFIGS["llava_b1"].with_(h_kv=2, rank=16, n_vis=211, n_text=5),
+    "r128": CONFIGS["llava_b1"].with_(h_kv=2, rank=128, n_vis=150, n_text=9),
+    "odd_r": CONFIGS["llava_b1"].with_(h_kv=2, head_dim=64, rank=5, n_vis=97, n_text=3),
+}
+
+
+# ------------------------------------------------------------------ G-dec
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("name", list(SMALL))
+@pytest.mark.parametrize("kernel", [0, 1])
+def test_decode_on_oracle_cache(rk, name, dtype, kernel):
+    cfg = SMALL[name].with_(dtype=dtype)
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, dtype)
+    ref = orc.decode(w["q"].f64(), Kt, w["V"].f64(), R, dmu,
+                     w["Ktext"].f64() if cfg.n_text else None,
+                     w["Vtext"].f64() if cfg.n_text else None)
+    import torch
+    M = cfg.n_text
+    out = rk.decode_attn(to_torch(w["q"]), _as_dev(Kt, dtype), to_torch(w["V"]),
+                         torch.from_numpy(R.astype(np.float32)).cuda(),
+                         torch.from_numpy(dmu.astype(np.float32)).cuda(),
+                         to_torch(w["Ktext"]) if M else None, to_torch(w["Vtext"]) if M else None,
+                         kernel=kernel)
+    torch.cuda.synchronize()
+    err = max_rel_err(to_np64(out), ref)
+    assert err <= TOL[dtype], (name, dtype, kernel, err)
+
+
+@pytest.mark.parametrize("splits", [1, 2, 3, 7, 64])
+def test_decode_split_invariance(rk, splits):
+    """Split-K over the token axis is an exact re-association (App. C)."""
+    import torch
+    cfg = SMALL["qwen_small_r32"].with_(dtype="f32")
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, "f32")
+    args = (to_torch(w["q"]), _as_dev(Kt, "f32"), to_torch(w["V"]),
+            torch.from_numpy(R.astype(np.float32)).cuda(),
+            torch.from_numpy(dmu.astype(np.float32)).cuda(), to_torch(w["Ktext"]),
+            to_torch(w["Vtext"]))
+    base = rk.decode_attn(*args, splits=1, kernel=1)
+    out = rk.decode_attn(*args, splits=splits, kernel=1)
+    torch.cuda.synchronize()
+    assert max_rel_err(to_np64(out), to_np64(base)) < 2e-6
+
+
+def test_decode_single_token_and_zero_query(rk):
+    import torch
+    for kernel in (1, 2):
+        U, G, d, r = 2, 1, 128, 32
+        V = torch.randn(U, 1, d, device="cuda").bfloat16()
+        out = rk.decode_attn(torch.randn(U, G, d, device="cuda").bfloat16(),
+                             torch.randn(U, 1, r, device="cuda").bfloat16(), V,
+                             torch.randn(U, d, r, device="cuda"), torch.randn(U, d, device="cuda"),
+                             kernel=kernel)
+        torch.testing.assert_close(out[:, 0], V[:, 0].float(), rtol=0, atol=0)
+        N = 300
+        V = torch.randn(U, N, d, device="cuda").bfloat16()
+        out = rk.decode_attn(torch.zeros(U, G, d, device="cuda").bfloat16(),
+                             torch.randn(U, N, r, device="cuda").bfloat16(), V,
+                             torch.randn(U, d, r, device="cuda"), torch.randn(U, d, device="cuda"),
+                             kernel=kernel)
+        ref = V.double().mean(dim=1)
+        assert (out[:, 0].double() - ref).abs().max().item() < 1e-5
+
+
+def test_decode_deterministic_and_graph_replay(rk):
+    import torch
+    cfg = SMALL["llava_small"]
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, "bf16")
+    args = (to_torch(w["q"]), _as_dev(Kt, "bf16"), to_torch(w["V"]),
+            torch.from_numpy(R.astype(np.float32)).cuda(),
+            torch.from_numpy(dmu.astype(np.float32)).cuda(), to_torch(w["Ktext"]),
+            to_torch(w["Vtext"]))
+    a = rk.decode_attn(*args).clone()
+    out = torch.empty_like(a)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ws = rk.workspace(rk.make_dims(cfg.units, cfg.group, 128, cfg.rank, cfg.n_vis, cfg.n_text,
+                                       0, rk.BF16), rk.OP_DECODE, "cuda")
+        rk.decode_attn(*args, out=out, ws=ws)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            rk.decode_attn(*args, out=out, ws=ws)
+    for _ in range(3):
+        out.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        assert torch.equal(out, a)
+
+
+# ------------------------------------------------------------------ G-sel
+def _sel_cases():
+    rng = np.random.default_rng(5)
+    d = 128
+    cases = {
+        "random": rng.standard_normal((4, d)),
+        "ties": rng.integers(0, 6, (4, d)).astype(float),
+        "all_equal": np.full((2, d), 3.0),
+        "signed_zero": np.where(rng.random((2, d)) < 0.5, 0.0, -0.0),
+        "denormal": rng.integers(0, 3, (2, d)) * np.float64(np.float32(1e-45)),
+    }
+    straddle = np.sort(rng.standard_normal(d))[::-1].copy()
+    straddle[30:36] = straddle[30]  # ties straddling rank 32
+    cases["straddle"] = straddle[None]
+    return cases
+
+
+@pytest.mark.parametrize("case", list(_sel_cases()))
+@pytest.mark.parametrize("r", [1, 31, 32, 33, 128])
+def test_select_bit_exact(rk, case, r):
+    import torch
+    lam = _sel_cases()[case].astype(np.float32)
+    mask, idx, info = rk.select_topr(torch.from_numpy(lam).cuda(), r)
+    torch.cuda.synchronize()
+    for u in range(lam.shape[0]):
+        om, oi = orc.select_topr(lam[u].astype(np.float64), r)
+        np.testing.assert_array_equal(mask_bits_u32(mask[u].cpu().numpy()), om)
+        np.testing.assert_array_equal(idx[u].cpu().numpy(), oi)
+        assert info[u].item() == 0
+
+
+def test_select_nan(rk):
+    import torch
+    lam = np.ones((2, 64), dtype=np.float32)
+    lam[1, 7] = np.nan
+    mask, idx, info = rk.select_topr(torch.from_numpy(lam).cuda(), 8)
+    assert info.tolist() == [0, -1]
+    assert (idx[1] == -1).all() and (mask[1] == 0).all()
+
+
+# ------------------------------------------------------------------ G-cal / G-cmp
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("mean", [0.5, 20.0])
+def test_calibrate_gap_data(rk, dtype, mean):
+    import torch
+    cfg = CONFIGS["llava_b1"].with_(h_kv=4, n_vis=777, n_text=0, dtype=dtype)
+    w = make_workload(cfg, dist="gap", mean=mean)
+    K = to_torch(w["K"])
+    cal = rk.calibrate(K, to_torch(w["Qw"]), cfg.rank, want_full=True)
+    torch.cuda.synchronize()
+    ref = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
+    R = to_np64(cal["R"])
+    lam = to_np64(cal["eigvals"])
+    assert (cal["info"].cpu().numpy() == 0).all()
+    for u in range(cfg.units):
+        P = R[u] @ R[u].T
+        Pref = ref["R"][u] @ ref["R"][u].T
+        assert np.linalg.norm(P - Pref) <= 1e-3, u
+        assert np.linalg.norm(R[u].T @ R[u] - np.eye(cfg.rank)) <= 1e-3
+        Cq = ref["Cq"][u]
+        nrm = np.linalg.norm(Cq)
+        D = R[u].T @ Cq @ R[u]
+        assert np.linalg.norm(D - np.diag(np.diag(D))) / nrm <= 1e-5
+        assert abs(lam[u].sum() - np.trace(Cq)) <= 1e-5 * abs(np.trace(Cq)) + 1e-6 * nrm
+        captured = np.trace(D) / np.sort(ref["lam"][u])[-cfg.rank:].sum()
+        assert captured >= 1 - 1e-5
+        # select on the GPU's own eigenvalues is bit-exact with the oracle rule
+        om, oi = orc.select_topr(lam[u], cfg.rank)
+        np.testing.assert_array_equal(cal["idx"][u].cpu().numpy(), oi)
+        np.testing.assert_array_equal(mask_bits_u32(cal["mask"][u].cpu().numpy()), om)
+    # delta_mu from the stored R
+    dmu_ref = orc.dmu_from_R(R, ref["mu"])
+    np.testing.assert_allclose(to_np64(cal["dmu"]), dmu_ref, atol=2e-5 * max(1.0, mean), rtol=1e-5)
+    # G-cmp: K~ equals RNE(K R) of the GPU's own R up to fp32 accumulation order:
+    # |err| <= 1 ulp(dtype) of the value + 64 eps_f32 sum_i |K_i R_ik| (rounding-boundary
+    # flips are allowed, cancellation near zero is bounded by the absolute term)
+    Kc = rk.compress_kv(K, cal["R"])
+    torch.cuda.synchronize()
+    Kf = w["K"].f64()
+    want = orc.quantize(orc.compress(Kf, R), dtype)
+    got = to_np64(Kc)
+    absdot = np.einsum("uni,uir->unr", np.abs(Kf), np.abs(R))
+    ulp = 2.0 ** -7 if dtype == "bf16" else 2.0 ** -23
+    assert np.all(np.abs(got - want) <= ulp * np.abs(want) + 64 * 2.0 ** -24 * absdot)
+    if dtype == "bf16":
+        assert np.mean(got == want) > 0.999
+
+
+# ------------------------------------------------------------------ G-e2e
+E2E = {
+    "toy": CONFIGS["toy"],
+    "llava_small": SMALL["llava_small"],
+    "qwen_small": SMALL["qwen_small_r32"],
+    "qwen_small_r64": SMALL["qwen_small_r64"].with_(n_text=12),
+}
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+@pytest.mark.parametrize("name", list(E2E))
+def test_end_to_end(rk, name, dtype):
+    import torch
+    cfg = E2E[name].with_(dtype=dtype)
+    w = make_workload(cfg)
+    M = cfg.n_text
+    K = to_torch(w["K"])
+    cal = rk.calibrate(K, to_torch(w["Qw"]), cfg.rank)
+    Kc = rk.compress_kv(K, cal["R"])
+    out = rk.decode_attn(to_torch(w["q"]), Kc, to_torch(w["V"]), cal["R"], cal["dmu"],
+                         to_torch(w["Ktext"]) if M else None, to_torch(w["Vtext"]) if M else None)
+    torch.cuda.synchronize()
+    ref = orc.pipeline(w["K"].f64(), w["V"].f64(), w["Qw"].f64(), w["q"].f64(), cfg.rank, dtype,
+                       w["Ktext"].f64() if M else None, w["Vtext"].f64() if M else None)
+    err = max_rel_err(to_np64(out), ref["out"])
+    assert err <= TOL[dtype], (name, dtype, err)
+
+
+def test_toy_multi_step_decode(rk):
+    """configs[0]: 8 decode steps; step t appends (k_t, v_t) to the full-d segment and
+    attends with q_t (reading Q18)."""
+    import torch
+    cfg = CONFIGS["toy"]
+    w = make_workload(cfg)
+    rng = np.random.default_rng(123)
+    K = to_torch(w["K"])
+    cal = rk.calibrate(K, to_torch(w["Qw"]), cfg.rank)
+    Kc = rk.compress_kv(K, cal["R"])
+    ref_cal = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
+    Kt_ref = orc.quantize(orc.compress(w["K"].f64(), ref_cal["R"]), "bf16")
+    kx = np.zeros((1, 0, 16))
+    vx = np.zeros((1, 0, 16))
+    for t in range(8):
+        new = orc.quantize(rng.standard_normal((3, 1, 1, 16)), "bf16")
+        q, kx, vx = new[0], np.concatenate([kx, new[1]], 1), np.concatenate([vx, new[2]], 1)
+        out = rk.decode_attn(_as_dev(q, "bf16"), Kc, to_torch(w["V"]), cal["R"], cal["dmu"],
+                             _as_dev(kx, "bf16"), _as_dev(vx, "bf16"))
+        ref = orc.decode(q, Kt_ref, w["V"].f64(), ref_cal["R"], ref_cal["dmu"], kx, vx)
+        assert max_rel_err(to_np64(out), ref) <= 2e-3, t
+
+
+def test_nonfinite_input_sets_info(rk):
+    import torch
+    cfg = SMALL["llava_small"]
+    w = make_workload(cfg)
+    K = to_torch(w["K"]).clone()
+    K[1, 5, 3] = float("nan")
+    cal = rk.calibrate(K, to_torch(w["Qw"]), cfg.rank)
+    torch.cuda.synchronize()
+    info = cal["info"].cpu().tolist()
+    assert info[1] == -1 and info[0] == 0 and info[2] == 0
+    assert (cal["R"][1] == 0).all() and (cal["idx"][1] == -1).all()
+
+
+# ------------------------------------------------------------------ full size, sampled
+@pytest.mark.parametrize("name,sample", [("llava_b32", [0, 517, 1023]),
+                                         ("qwen_b32_r32", [0, 77, 127]),
+                                         ("long_b16", [5, 63])])
+def test_full_size_sampled(rk, name, sample):
+    """BASELINE.json full sizes in the launch configuration bench.py times; the oracle
+    recomputes sampled units one by one from the same seeded bytes."""
+    import torch
+    cfg = CONFIGS[name]
+    w = make_workload(cfg, threads=16)
+    M = cfg.n_text
+    K = to_torch(w["K"])
+    cal = rk.calibrate(K, to_torch(w["Qw"]), cfg.rank)
+    Kc = rk.compress_kv(K, cal["R"])
+    out = rk.decode_attn(to_torch(w["q"]), Kc, to_torch(w["V"]), cal["R"], cal["dmu"],
+                         to_torch(w["Ktext"]), to_torch(w["Vtext"]))
+    torch.cuda.synchronize()
+    assert (cal["info"].cpu().numpy() >= 0).all()
+    sub = make_workload(cfg, units=sample)
+    ref = orc.pipeline(sub["K"].f64(), sub["V"].f64(), sub["Qw"].f64(), sub["q"].f64(), cfg.rank,
+                       "bf16", sub["Ktext"].f64(), sub["Vtext"].f64())
+    err = max_rel_err(to_np64(out[sample]), ref["out"])
+    assert err <= 2e-3, (name, err)
+    # decode-only gate on the exact GPU bytes for the same units
+    idx = torch.tensor(sample, device="cuda")
+    ref_dec = orc.decode(sub["q"].f64(), to_np64(Kc[idx]), sub["V"].f64(), to_np64(cal["R"][idx]),
+                         to_np64(cal["dmu"][idx]), sub["Ktext"].f64(), sub["Vtext"].f64())
+    assert max_rel_err(to_np64(out[sample]), ref_dec) <= 1e-4
