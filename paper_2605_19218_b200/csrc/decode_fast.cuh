@@ -1,0 +1,451 @@
+// decode_fast.cuh -- the streaming decode kernel (d = 128), included by decode.cu.
+//
+// Work decomposition: the U*(N+M) tokens of the whole batch (unit-major; within a unit
+// the N visual tokens, then the M full-d text tokens) are cut into NW equal contiguous
+// ranges, one per WARP.  Every warp is an independent streaming worker:
+//   * lane 0 keeps STAGES tiles in flight in the warp's private shared-memory ring with
+//     1-D TMA bulk copies (cp.async.bulk.shared::cluster.global.mbarrier::complete_tx,
+//     SASS UBLKCP), the K~ (or K_text) tile then the V tile, both contiguous in HBM;
+//   * the warp computes the tile: scores with lane groups of 32 bytes of a key row
+//     (LPT lanes per token, shuffle-reduced), one online-softmax rescale per tile,
+//     probabilities broadcast through shared memory, P.V with each lane owning 4 of the
+//     128 value channels (two accumulator sets to halve the FMA dependency chains);
+//   * tiles never straddle a unit or segment boundary; at a unit change the warp
+//     flushes (m, l, acc) -- directly to `out` if it owns the whole unit, else as a
+//     partial -- and the last contributor of the unit (atomic ticket) merges the
+//     partials in slot order (deterministic) and re-arms the ticket.
+// No CTA-level barrier exists anywhere; the CTA is only a container of WARPS warps.
+
+constexpr int kD = 128;
+
+template <typename T, int RK, int G, int WARPS, int STAGES, int TTV>
+struct FastCfg {
+  static constexpr int S = sizeof(T);
+  static constexpr int CHB = 32;                       // bytes of a key row per lane
+  static constexpr int CHN = CHB / S;                  // channels per lane chunk
+  static constexpr int LPT_V = RK * S / CHB;           // lanes per visual token
+  static constexpr int LPT_X = kD * S / CHB;           // lanes per text token
+  static constexpr int TPS_V = 32 / LPT_V;             // visual tokens per step
+  static constexpr int TPS_X = 32 / LPT_X;
+  static constexpr int TT_V = TTV;                     // visual tile tokens
+  static constexpr int STAGE = TT_V * (RK + kD) * S;   // bytes per stage
+  static constexpr int XQ = (TPS_X > 4 ? TPS_X : 4);   // text tile granule (lcm(TPS_X, 4))
+  static constexpr int TT_X = ((STAGE / (2 * kD * S)) / XQ) * XQ;
+  static constexpr int TT_P = TT_V > TT_X ? TT_V : TT_X;
+  static constexpr int VPL = kD / 32;                  // V channels per lane (4)
+  static constexpr int NACC = (G == 1) ? 2 : 1;        // accumulator sets
+  // per-warp shared memory
+  static constexpr int OFF_Q = STAGES * STAGE;                    // float [G][kD]  scaled q
+  static constexpr int OFF_QT = OFF_Q + G * kD * 4;              // float [G][RK]  scaled q~
+  static constexpr int OFF_P = OFF_QT + G * RK * 4;              // float [G][TT_P] probabilities
+  static constexpr int OFF_B = OFF_P + G * TT_P * 4;             // float [G] bias (pad 16 B)
+  static constexpr int OFF_BAR = (OFF_B + ((G + 3) / 4) * 16 + 7) / 8 * 8;
+  static constexpr int WARP_SMEM = ((OFF_BAR + STAGES * 8) + 127) / 128 * 128;
+  static constexpr int SMEM = WARPS * WARP_SMEM;
+  static_assert(LPT_V >= 1 && LPT_V <= 32 && (32 % LPT_V) == 0, "bad RK");
+  static_assert(TT_X >= XQ && TT_X % 4 == 0, "text tile too small");
+  static_assert(TT_V % TPS_V == 0 && TT_V % 4 == 0, "tile");
+  static_assert(STAGE % 16 == 0, "stage alignment");
+};
+
+__device__ __forceinline__ long long range_start(long long T, int gw, int NW) {
+  return T * gw / NW;
+}
+// warp whose range contains global token x
+__device__ __forceinline__ int warp_of(long long x, long long T, int NW) {
+  int g = (int)(x * NW / T);
+  while (g + 1 < NW && range_start(T, g + 1, NW) <= x) ++g;
+  while (g > 0 && range_start(T, g, NW) > x) --g;
+  return g;
+}
+
+struct Tile {
+  int u;      // unit
+  int vis;    // 1 visual, 0 text
+  int t;      // first token within the segment
+  int tn;     // tokens in this tile
+};
+
+template <int TT_V, int TT_X>
+__device__ __forceinline__ Tile tile_at(long long x, long long b, int N, int M) {
+  const long long L = (long long)N + M;
+  Tile tl;
+  tl.u = (int)(x / L);
+  const int off = (int)(x - (long long)tl.u * L);
+  long long e;
+  if (off < N) {
+    tl.vis = 1; tl.t = off;
+    const long long seg_end = (long long)tl.u * L + N;
+    e = x + TT_V;
+    if (e > seg_end) e = seg_end;
+  } else {
+    tl.vis = 0; tl.t = off - N;
+    const long long seg_end = (long long)(tl.u + 1) * L;
+    e = x + TT_X;
+    if (e > seg_end) e = seg_end;
+  }
+  if (e > b) e = b;
+  tl.tn = (int)(e - x);
+  return tl;
+}
+
+template <typename T>
+__device__ __forceinline__ void unpack_chunk(const unsigned char* p, float* f);  // 32 bytes
+template <>
+__device__ __forceinline__ void unpack_chunk<__nv_bfloat16>(const unsigned char* p, float* f) {
+  const uint4 a = *reinterpret_cast<const uint4*>(p);
+  const uint4 b = *reinterpret_cast<const uint4*>(p + 16);
+  const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int i = 0; i < 8; ++i) { f[2 * i] = bf16lo(w[i]); f[2 * i + 1] = bf16hi(w[i]); }
+}
+template <>
+__device__ __forceinline__ void unpack_chunk<float>(const unsigned char* p, float* f) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  const float4 b = *reinterpret_cast<const float4*>(p + 16);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w; f[4] = b.x; f[5] = b.y; f[6] = b.z; f[7] = b.w;
+}
+
+template <typename T>
+__device__ __forceinline__ void load_v4(const unsigned char* p, float* f);
+template <>
+__device__ __forceinline__ void load_v4<__nv_bfloat16>(const unsigned char* p, float* f) {
+  const uint2 a = *reinterpret_cast<const uint2*>(p);
+  f[0] = bf16lo(a.x); f[1] = bf16hi(a.x); f[2] = bf16lo(a.y); f[3] = bf16hi(a.y);
+}
+template <>
+__device__ __forceinline__ void load_v4<float>(const unsigned char* p, float* f) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+}
+
+// One tile: scores (key rows of KR channels), online-softmax rescale, P.V.
+// FULL: tn == TT (branch-free, fully unrolled); else the tail path.
+template <typename T, int KR, int TT, int G, int NACC, bool FULL, bool BIAS>
+__device__ __forceinline__ void tile_compute(const unsigned char* __restrict__ kbuf,
+                                             const unsigned char* __restrict__ vbuf, int tn,
+                                             const float* __restrict__ qsm,
+                                             const float (&qreg)[32 / sizeof(T)],
+                                             const float* __restrict__ bs, float* __restrict__ pbuf,
+                                             float (&m)[G], float (&l)[G],
+                                             float (&acc)[NACC][G][4], int lane) {
+  constexpr int S = sizeof(T);
+  constexpr int CHN = 32 / S;
+  constexpr int LPT = KR * S / 32;
+  constexpr int TPS = 32 / LPT;
+  constexpr int NS = TT / TPS;
+  const int cv = lane % LPT, tv = lane / LPT;
+  float sc[G][NS];
+#pragma unroll
+  for (int s = 0; s < NS; ++s) {
+    const int tok = s * TPS + tv;
+    float kf[CHN];
+    unpack_chunk<T>(kbuf + (size_t)tok * KR * S + cv * 32, kf);
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float d0 = 0.f, d1 = 0.f;
+      if constexpr (G == 1) {
+#pragma unroll
+        for (int i = 0; i < CHN; i += 2) {
+          d0 = fmaf(qreg[i], kf[i], d0);
+          d1 = fmaf(qreg[i + 1], kf[i + 1], d1);
+        }
+      } else {
+        const float* qq = qsm + g * KR + cv * CHN;
+#pragma unroll
+        for (int i = 0; i < CHN; i += 4) {
+          const float4 q4 = *reinterpret_cast<const float4*>(qq + i);
+          d0 = fmaf(q4.x, kf[i], d0);
+          d1 = fmaf(q4.y, kf[i + 1], d1);
+          d0 = fmaf(q4.z, kf[i + 2], d0);
+          d1 = fmaf(q4.w, kf[i + 3], d1);
+        }
+      }
+      float dsum = d0 + d1;
+#pragma unroll
+      for (int o = 1; o < LPT; o <<= 1) dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+      if constexpr (BIAS) dsum += bs[g];
+      sc[g][s] = (FULL || tok < tn) ? dsum : -CUDART_INF_F;
+    }
+  }
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    float tmax = sc[g][0];
+#pragma unroll
+    for (int s = 1; s < NS; ++s) tmax = fmaxf(tmax, sc[g][s]);
+#pragma unroll
+    for (int o = 16; o >= LPT; o >>= 1) tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    const float mn = fmaxf(m[g], tmax);
+    const float alpha = fast_exp2(m[g] - mn);
+    m[g] = mn;
+    l[g] *= alpha;
+#pragma unroll
+    for (int a = 0; a < NACC; ++a)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[a][g][k] *= alpha;
+#pragma unroll
+    for (int s = 0; s < NS; ++s) {
+      const float pr = fast_exp2(sc[g][s] - mn);
+      if (cv == 0) {
+        l[g] += pr;
+        pbuf[g * TT + s * TPS + tv] = pr;
+      }
+    }
+  }
+  __syncwarp();
+  if constexpr (FULL) {
+#pragma unroll
+    for (int t4 = 0; t4 < TT / 4; ++t4) {
+      float4 pg[G];
+#pragma unroll
+      for (int g = 0; g < G; ++g) pg[g] = *reinterpret_cast<const float4*>(pbuf + g * TT + 4 * t4);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float vf[4];
+        load_v4<T>(vbuf + (size_t)(4 * t4 + j) * kD * S + lane * 4 * S, vf);
+        const int a = j % NACC;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const float pj = j == 0 ? pg[g].x : j == 1 ? pg[g].y : j == 2 ? pg[g].z : pg[g].w;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc[a][g][k] = fmaf(pj, vf[k], acc[a][g][k]);
+        }
+      }
+    }
+  } else {
+    for (int t = 0; t < tn; ++t) {
+      float vf[4];
+      load_v4<T>(vbuf + (size_t)t * kD * S + lane * 4 * S, vf);
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float pj = pbuf[g * TT + t];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[0][g][k] = fmaf(pj, vf[k], acc[0][g][k]);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+template <typename T, int RK, int G, int WARPS, int STAGES, int TTV, int MINB>
+__global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodeParams p, int NW, int cmax) {
+  using C = FastCfg<T, RK, G, WARPS, STAGES, TTV>;
+  constexpr int NACC = C::NACC;
+  extern __shared__ __align__(128) unsigned char fsm[];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * WARPS + w;
+  if (gw >= NW) return;
+  unsigned char* base = fsm + w * C::WARP_SMEM;
+  float* qs = reinterpret_cast<float*>(base + C::OFF_Q);
+  float* qts = reinterpret_cast<float*>(base + C::OFF_QT);
+  float* pbuf = reinterpret_cast<float*>(base + C::OFF_P);
+  float* bs = reinterpret_cast<float*>(base + C::OFF_B);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
+
+  const int N = p.N, M = p.M;
+  const long long L = (long long)N + M;
+  const long long Ttot = L * p.U;
+  const long long a = range_start(Ttot, gw, NW), b = range_start(Ttot, gw + 1, NW);
+  if (a >= b) return;
+
+  const T* Kc = static_cast<const T*>(p.Kc);
+  const T* V = static_cast<const T*>(p.V);
+  const T* Kt = static_cast<const T*>(p.Kt);
+  const T* Vt = static_cast<const T*>(p.Vt);
+  const uint64_t pol = policy_evict_first();
+
+  if (lane == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  __syncwarp();
+
+  // ---------------- producer (lane 0): issue the tile at cursor px into stage st
+  long long px = a;
+  auto issue = [&](int st) {
+    const Tile tl = tile_at<C::TT_V, C::TT_X>(px, b, N, M);
+    unsigned char* dst = base + st * C::STAGE;
+    if (tl.vis) {
+      const uint32_t kb = (uint32_t)tl.tn * RK * C::S, vb = (uint32_t)tl.tn * kD * C::S;
+      mbar_arrive_expect_tx(&bar[st], kb + vb);
+      bulk_g2s(dst, Kc + ((size_t)tl.u * N + tl.t) * RK, kb, &bar[st], pol);
+      bulk_g2s(dst + C::TT_V * RK * C::S, V + ((size_t)tl.u * N + tl.t) * kD, vb, &bar[st], pol);
+    } else {
+      const uint32_t kb = (uint32_t)tl.tn * kD * C::S;
+      mbar_arrive_expect_tx(&bar[st], 2 * kb);
+      bulk_g2s(dst, Kt + ((size_t)tl.u * M + tl.t) * kD, kb, &bar[st], pol);
+      bulk_g2s(dst + C::TT_X * kD * C::S, Vt + ((size_t)tl.u * M + tl.t) * kD, kb, &bar[st], pol);
+    }
+    px += tl.tn;
+  };
+  if (lane == 0)
+    for (int s = 0; s < STAGES && px < b; ++s) issue(s);
+
+  // ---------------- consumer state
+  float m[G], l[G], acc[NACC][G][4];
+  float qreg[C::CHN], xreg[C::CHN];  // register copies of q~ / q chunks when G == 1
+  int cur_u = -1;
+
+  auto setup = [&](int u) {
+    // q (fp32) -> smem; q~ = q R_r and b = q . dmu (Alg. 2 l.1-2); then scale by sl
+    const T* qg = static_cast<const T*>(p.q) + (size_t)u * G * kD;
+    for (int e = lane; e < G * kD; e += 32) qs[e] = Elem<T>::to_f(qg[e]);
+    __syncwarp();
+    const float* Ru = p.R + (size_t)u * kD * RK;
+    constexpr int KPL = (RK + 31) / 32;
+    float qa[G][KPL];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) qa[g][j] = 0.f;
+#pragma unroll 4
+    for (int i = 0; i < kD; ++i) {
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int k = lane + 32 * j;
+        const float rv = (k < RK) ? __ldg(Ru + (size_t)i * RK + k) : 0.f;
+#pragma unroll
+        for (int g = 0; g < G; ++g) qa[g][j] = fmaf(qs[g * kD + i], rv, qa[g][j]);
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const int k = lane + 32 * j;
+        if (k < RK) qts[g * RK + k] = qa[g][j] * p.sl;
+      }
+      float bb = 0.f;
+      if (p.dmu) {
+#pragma unroll
+        for (int j = 0; j < kD / 32; ++j)
+          bb = fmaf(qs[g * kD + lane + 32 * j], __ldg(p.dmu + (size_t)u * kD + lane + 32 * j), bb);
+      }
+      bb = warp_sum(bb);
+      if (lane == 0) bs[g] = bb * p.sl;
+    }
+    __syncwarp();
+    for (int e = lane; e < G * kD; e += 32) qs[e] *= p.sl;
+    __syncwarp();
+    if constexpr (G == 1) {
+      const int cv = lane % C::LPT_V, cx = lane % C::LPT_X;
+#pragma unroll
+      for (int i = 0; i < C::CHN; ++i) {
+        qreg[i] = qts[cv * C::CHN + i];
+        xreg[i] = qs[cx * C::CHN + i];
+      }
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      m[g] = -CUDART_INF_F;
+      l[g] = 0.f;
+#pragma unroll
+      for (int aa = 0; aa < NACC; ++aa)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[aa][g][k] = 0.f;
+    }
+  };
+
+  auto flush = [&](int u) {
+    const long long x0 = (long long)u * L, x1 = x0 + L - 1;
+    const int first = warp_of(x0, Ttot, NW), last = warp_of(x1, Ttot, NW);
+    const int count = last - first + 1;
+    float lt[G], A[G][4];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      lt[g] = warp_sum(l[g]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        A[g][k] = acc[0][g][k];
+#pragma unroll
+        for (int aa = 1; aa < NACC; ++aa) A[g][k] += acc[aa][g][k];
+      }
+    }
+    if (count == 1) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        const float inv = 1.f / lt[g];
+        *reinterpret_cast<float4*>(p.out + ((size_t)u * G + g) * kD + lane * 4) =
+            make_float4(A[g][0] * inv, A[g][1] * inv, A[g][2] * inv, A[g][3] * inv);
+      }
+      return;
+    }
+    // partial record: acc[kD] | m | l | pad[2]  (stride kRec floats, 16-byte aligned)
+    constexpr int kRec = kD + 4;
+    const int slot = gw - first;
+    float* part = p.partials + ((size_t)u * cmax) * G * kRec;
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float* dst = part + ((size_t)slot * G + g) * kRec;
+      if (lane == 0) { dst[kD] = m[g]; dst[kD + 1] = lt[g]; }
+      *reinterpret_cast<float4*>(dst + lane * 4) = make_float4(A[g][0], A[g][1], A[g][2], A[g][3]);
+    }
+    __threadfence();
+    __syncwarp();
+    unsigned prev = 0;
+    if (lane == 0) prev = atomicAdd(&p.counters[u], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != (unsigned)(count - 1)) return;
+    __threadfence();
+#pragma unroll 1
+    for (int g = 0; g < G; ++g) {
+      float Mx = -CUDART_INF_F;
+      for (int s = 0; s < count; ++s) Mx = fmaxf(Mx, __ldcg(part + ((size_t)s * G + g) * kRec + kD));
+      float Ls = 0.f, R4[4] = {0.f, 0.f, 0.f, 0.f};
+      for (int s = 0; s < count; ++s) {
+        const float* src = part + ((size_t)s * G + g) * kRec;
+        const float ms = __ldcg(src + kD);
+        const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx);
+        Ls = fmaf(__ldcg(src + kD + 1), f, Ls);
+        const float4 v = __ldcg(reinterpret_cast<const float4*>(src + lane * 4));
+        R4[0] = fmaf(v.x, f, R4[0]); R4[1] = fmaf(v.y, f, R4[1]);
+        R4[2] = fmaf(v.z, f, R4[2]); R4[3] = fmaf(v.w, f, R4[3]);
+      }
+      const float inv = 1.f / Ls;
+      *reinterpret_cast<float4*>(p.out + ((size_t)u * G + g) * kD + lane * 4) =
+          make_float4(R4[0] * inv, R4[1] * inv, R4[2] * inv, R4[3] * inv);
+    }
+    if (lane == 0) p.counters[u] = 0u;
+  };
+
+  // ---------------- main loop over this warp's tiles
+  long long cx = a;
+  int j = 0;
+  while (cx < b) {
+    const Tile tl = tile_at<C::TT_V, C::TT_X>(cx, b, N, M);
+    const int st = j % STAGES;
+    const uint32_t ph = (uint32_t)((j / STAGES) & 1);
+    if (tl.u != cur_u) {
+      if (cur_u >= 0) flush(cur_u);
+      setup(tl.u);
+      cur_u = tl.u;
+    }
+    mbar_wait(&bar[st], ph);
+    const unsigned char* kbuf = base + st * C::STAGE;
+    if (tl.vis) {
+      const unsigned char* vbuf = kbuf + C::TT_V * RK * C::S;
+      if (tl.tn == C::TT_V)
+        tile_compute<T, RK, C::TT_V, G, NACC, true, true>(kbuf, vbuf, tl.tn, qts, qreg, bs, pbuf,
+                                                          m, l, acc, lane);
+      else
+        tile_compute<T, RK, C::TT_V, G, NACC, false, true>(kbuf, vbuf, tl.tn, qts, qreg, bs, pbuf,
+                                                           m, l, acc, lane);
+    } else {
+      const unsigned char* vbuf = kbuf + C::TT_X * kD * C::S;
+      if (tl.tn == C::TT_X)
+        tile_compute<T, kD, C::TT_X, G, NACC, true, false>(kbuf, vbuf, tl.tn, qs, xreg, bs, pbuf,
+                                                           m, l, acc, lane);
+      else
+        tile_compute<T, kD, C::TT_X, G, NACC, false, false>(kbuf, vbuf, tl.tn, qs, xreg, bs, pbuf,
+                                                            m, l, acc, lane);
+    }
+    // refill this stage with the tile STAGES ahead (the whole warp has consumed it)
+    if (lane == 0 && px < b) {
+      fence_proxy_async();
+      issue(st);
+    }
+    cx += tl.tn;
+    ++j;
+  }
+  if (cur_u >= 0) flush(cur_u);
+}
