@@ -70,7 +70,9 @@ def peaks():
 
 
 def rank_units(cfg, rank):
-    return list(range(rank * cfg.units, (rank + 1) * cfg.units))
+    """Weak scaling: each rank owns a full per-GPU batch of units (sharding.weak_units)."""
+    from paper_2605_19218_b200.sharding import weak_units
+    return list(weak_units(cfg.units, rank))
 
 
 # ----------------------------------------------------------------------------- CPU oracle
