@@ -73,6 +73,8 @@ enum {
                                      (faster; projector error ~1e-4, which can exceed
                                      the 2e-3 end-to-end gate on some data).  Default:
                                      fp64 Jacobi (projector error ~1e-7)               */
+  ROTATEK_SIMT_ONLY = 1u << 8,    /* use the CUDA-core (SIMT) kernels instead of the tcgen05
+                                     tensor-core ones (A/B tests and benches)           */
   ROTATEK_DEFAULT_FLAGS = (1u << 0) | (1u << 1)
 };
 

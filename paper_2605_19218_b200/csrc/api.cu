@@ -100,7 +100,9 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const v
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int n = 0;
   if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
-  if ((s = launched(rk::launch_cov(U, N, d, bf16, K, ws, st), &n))) return s;
+  const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::cov_tc_supported(d, bf16);
+  if ((s = launched(tc ? rk::launch_cov_tc(U, N, K, ws, st) : rk::launch_cov(U, N, d, bf16, K, ws, st), &n)))
+    return s;
   if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
   if ((s = launched(rk::launch_jacobi(U, d, fp64, ws, st), &n))) return s;
   if ((s = launched(rk::launch_select_gather(U, d, r, fp64, bf16, center, ws, R, dmu, eigvals,

@@ -36,6 +36,8 @@ size_t decode_ws_layout(int U, int G, int d, int N, int M, void* base, DecodeWs*
 int launch_sigma(int U, int G, int W, int d, bool bf16, bool weight, const void* Qw,
                  double* sigma, cudaStream_t st);
 int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws, cudaStream_t st);
+bool cov_tc_supported(int d, bool bf16);
+int launch_cov_tc(int U, int N, const void* K, const CalibWs& ws, cudaStream_t st);
 int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st);
 int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st);
 int launch_select_gather(int U, int d, int r, bool fp64_vecs, bool bf16x2, bool center,

@@ -326,3 +326,36 @@ def test_full_size_sampled(rk, name, sample):
     ref_dec = orc.decode(sub["q"].f64(), to_np64(Kc[idx]), sub["V"].f64(), to_np64(cal["R"][idx]),
                          to_np64(cal["dmu"][idx]), sub["Ktext"].f64(), sub["Vtext"].f64())
     assert max_rel_err(to_np64(out[sample]), ref_dec) <= 1e-4
+
+
+# ------------------------------------------------------------------ tcgen05 vs CUDA-core paths
+@pytest.mark.parametrize("h_kv,n_vis", [(3, 777), (40, 300), (1, 4096), (2, 129)])
+def test_calibrate_tensor_core_matches_simt(rk, h_kv, n_vis):
+    """The tcgen05 covariance (TMA + TMEM, 128-token fp32 windows) and the CUDA-core one
+    agree; both are checked against the oracle's eigen-basis."""
+    import torch
+    cfg = CONFIGS["llava_b1"].with_(h_kv=h_kv, n_vis=n_vis, n_text=0)
+    w = make_workload(cfg, dist="gap", mean=5.0)
+    K, Qw = to_torch(w["K"]), to_torch(w["Qw"])
+    a = rk.calibrate(K, Qw, cfg.rank)
+    b = rk.calibrate(K, Qw, cfg.rank, rk.DEFAULT_FLAGS | rk.SIMT_ONLY)
+    torch.cuda.synchronize()
+    ref = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
+    la, lb = to_np64(a["eigvals"]), to_np64(b["eigvals"])
+    lr = ref["lam"]
+    # fp32 windows of keys with a mean offset: the absolute eigenvalue error is a small
+    # multiple of eps_f32 * N * |mu|^2 (one-pass S - N mu mu^T), relative to lambda_max
+    for lg in (la, lb):
+        err = np.abs(np.sort(lg, 1) - np.sort(lr, 1)).max(1) / np.abs(lr).max(1)
+        assert err.max() < 2e-5, err
+    Ra, Rb = to_np64(a["R"]), to_np64(b["R"])
+    for u in range(cfg.units):
+        Pa, Pb = Ra[u] @ Ra[u].T, Rb[u] @ Rb[u].T
+        Pr = ref["R"][u] @ ref["R"][u].T
+        assert np.linalg.norm(Pa - Pr) < 1e-4, (u, np.linalg.norm(Pa - Pr))
+        assert np.linalg.norm(Pb - Pr) < 1e-4, (u, np.linalg.norm(Pb - Pr))
+    # delta_mu of each path equals (I - R R^T) mu for that path's own stored R (P:982)
+    for cal, R in ((a, Ra), (b, Rb)):
+        want = orc.dmu_from_R(R, ref["mu"])
+        scale = np.linalg.norm(ref["mu"], axis=1, keepdims=True)
+        assert (np.abs(to_np64(cal["dmu"]) - want) / scale).max() < 1e-5
