@@ -139,6 +139,12 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dims, uint32_t flags, const
 rotatek_status rotatek_compress_kv(const rotatek_dims* dims, const void* K, const float* R,
                                    void* K_comp, rotatek_stream_t stream);
 
+/* Same, with flags: ROTATEK_SIMT_ONLY selects the CUDA-core kernel instead of the tcgen05
+ * one (d = 128, bf16, r in {16, 32, 64, 128}: R split exactly into three bf16 terms, fp32
+ * accumulation in TMEM).  Other flag bits are ignored. */
+rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dims, const void* K, const float* R,
+                                      void* K_comp, uint32_t flags, rotatek_stream_t stream);
+
 /*
  * Alg. 2 for all U*G query heads in one launch:
  *   q~ = q R_r ; b = q . dmu

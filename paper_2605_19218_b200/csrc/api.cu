@@ -112,8 +112,8 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const v
   return ROTATEK_OK;
 }
 
-rotatek_status rotatek_compress_kv(const rotatek_dims* dm, const void* K, const float* R,
-                                   void* K_comp, rotatek_stream_t stream) {
+rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dm, const void* K, const float* R,
+                                      void* K_comp, uint32_t flags, rotatek_stream_t stream) {
   g_launches = 0;
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
@@ -121,14 +121,23 @@ rotatek_status rotatek_compress_kv(const rotatek_dims* dm, const void* K, const 
   if (!aligned16(K) || !aligned16(R) || !aligned16(K_comp))
     return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
   const int d = dm->head_dim, r = dm->rank;
-  if (((size_t)d * r + 64 * (size_t)d) * 4 > 227 * 1024)
+  const bool bf16 = dm->dtype == ROTATEK_BF16;
+  const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::compress_tc_supported(d, r, bf16);
+  if (!tc && ((size_t)d * r + 64 * (size_t)d) * 4 > 227 * 1024)
     return fail(ROTATEK_ERR_UNSUPPORTED, "compress: d*r too large");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int n = 0;
-  if ((s = launched(rk::launch_compress(dm->units, dm->n_vis, d, r, dm->dtype == ROTATEK_BF16, K, R,
-                                        K_comp, reinterpret_cast<cudaStream_t>(stream)), &n)))
+  if ((s = launched(tc ? rk::launch_compress_tc(dm->units, dm->n_vis, r, K, R, K_comp, st)
+                       : rk::launch_compress(dm->units, dm->n_vis, d, r, bf16, K, R, K_comp, st),
+                    &n)))
     return s;
   g_launches = n;
   return ROTATEK_OK;
+}
+
+rotatek_status rotatek_compress_kv(const rotatek_dims* dm, const void* K, const float* R,
+                                   void* K_comp, rotatek_stream_t stream) {
+  return rotatek_compress_kv_ex(dm, K, R, K_comp, 0u, stream);
 }
 
 rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dm, const void* q, const void* K_comp,

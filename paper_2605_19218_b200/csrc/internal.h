@@ -37,6 +37,8 @@ int launch_sigma(int U, int G, int W, int d, bool bf16, bool weight, const void*
                  double* sigma, cudaStream_t st);
 int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws, cudaStream_t st);
 bool cov_tc_supported(int d, bool bf16);
+bool compress_tc_supported(int d, int r, bool bf16);
+int launch_compress_tc(int U, int N, int r, const void* K, const float* R, void* Kc, cudaStream_t st);
 int launch_cov_tc(int U, int N, const void* K, const CalibWs& ws, cudaStream_t st);
 int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st);
 int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st);

@@ -61,11 +61,13 @@ def lib():
             L.rotatek_workspace_bytes.restype = sz
             L.rotatek_calibrate.argtypes = [dp, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
             L.rotatek_compress_kv.argtypes = [dp, vp, vp, vp, vp]
+            L.rotatek_compress_kv_ex.argtypes = [dp, vp, vp, vp, u32, vp]
             L.rotatek_decode_attn.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz, vp]
             L.rotatek_decode_attn_ex.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz,
                                                  i32, i32, vp]
             L.rotatek_select_topr.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp]
-            for fn in ("rotatek_calibrate", "rotatek_compress_kv", "rotatek_decode_attn",
+            for fn in ("rotatek_calibrate", "rotatek_compress_kv", "rotatek_compress_kv_ex",
+                       "rotatek_decode_attn",
                        "rotatek_decode_attn_ex", "rotatek_select_topr"):
                 getattr(L, fn).restype = ctypes.c_int
             L.rotatek_status_string.argtypes = [ctypes.c_int]
@@ -173,16 +175,17 @@ def calibrate(K: torch.Tensor, Qw: torch.Tensor | None, rank: int, flags: int = 
 
 # --------------------------------------------------------------------------- compress
 def compress_kv(K: torch.Tensor, R: torch.Tensor, out: torch.Tensor | None = None,
-                stream=None) -> torch.Tensor:
-    """Alg. 1 line 14: K~ = RNE(K R_r).  K [U, N, d], R [U, d, r] f32 -> [U, N, r] K.dtype."""
+                stream=None, flags: int = 0) -> torch.Tensor:
+    """Alg. 1 line 14: K~ = RNE(K R_r).  K [U, N, d], R [U, d, r] f32 -> [U, N, r] K.dtype.
+    flags: SIMT_ONLY selects the CUDA-core kernel instead of tcgen05."""
     U, N, d = K.shape
     r = R.shape[2]
     assert R.shape == (U, d, r) and R.dtype == torch.float32
     if out is None:
         out = torch.empty((U, N, r), dtype=K.dtype, device=K.device)
     dims = make_dims(U, 1, d, r, N, 0, 0, _dtype_code(K))
-    _check(lib().rotatek_compress_kv(ctypes.byref(dims), _ptr(K), _ptr(R), _ptr(out),
-                                     _stream(stream)))
+    _check(lib().rotatek_compress_kv_ex(ctypes.byref(dims), _ptr(K), _ptr(R), _ptr(out),
+                                        int(flags), _stream(stream)))
     return out
 
 

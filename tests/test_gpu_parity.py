@@ -359,3 +359,28 @@ def test_calibrate_tensor_core_matches_simt(rk, h_kv, n_vis):
         want = orc.dmu_from_R(R, ref["mu"])
         scale = np.linalg.norm(ref["mu"], axis=1, keepdims=True)
         assert (np.abs(to_np64(cal["dmu"]) - want) / scale).max() < 1e-5
+
+
+@pytest.mark.parametrize("r,h_kv,n_vis", [(32, 3, 777), (64, 2, 300), (16, 1, 129), (128, 2, 256),
+                                          (32, 300, 200)])
+def test_compress_tensor_core(rk, r, h_kv, n_vis):
+    """tcgen05 compress (R split exactly into 3 bf16 terms) vs RNE(K R) in fp64 and vs the
+    CUDA-core kernel: identical up to fp32 accumulation-order rounding flips."""
+    import torch
+    cfg = CONFIGS["llava_b1"].with_(h_kv=h_kv, n_vis=n_vis, rank=r, n_text=0)
+    w = make_workload(cfg, mean=3.0)
+    K = to_torch(w["K"])
+    rng = np.random.default_rng(r + n_vis)
+    R = np.stack([np.linalg.qr(rng.standard_normal((128, 128)))[0][:, :r] for _ in range(cfg.units)])
+    Rt = torch.from_numpy(R.astype(np.float32)).cuda()
+    a = rk.compress_kv(K, Rt)
+    b = rk.compress_kv(K, Rt, flags=rk.SIMT_ONLY)
+    torch.cuda.synchronize()
+    Kf = w["K"].f64()
+    R32 = R.astype(np.float32).astype(np.float64)
+    want = orc.quantize(orc.compress(Kf, R32), "bf16")
+    absdot = np.einsum("uni,uir->unr", np.abs(Kf), np.abs(R32))
+    for got in (to_np64(a), to_np64(b)):
+        assert np.all(np.abs(got - want) <= 2.0 ** -7 * np.abs(want) + 64 * 2.0 ** -24 * absdot)
+        assert np.mean(got == want) > 0.995
+    assert np.mean(to_np64(a) == to_np64(b)) > 0.995
