@@ -258,6 +258,7 @@ def run_ours(args):
     stream.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(stream):
         decode_step()
+        launches_per_decode = rk.last_launch_count()
         if not args.no_graph:
             graph = torch.cuda.CUDAGraph()
             with torch.cuda.graph(graph, stream=stream):
@@ -428,7 +429,8 @@ def run_ours(args):
         "e2e": e2e,
         "full_step": full,
         "clocks": clocks.summary(),
-        "gpu_launches": args.steps * L,
+        "gpu_launches": args.steps * L * launches_per_decode,
+        "launches_per_decode": launches_per_decode,
         "calibrate_info_nonzero": bad_info,
         "host_gen_s": round(t_gen, 1),
     }

@@ -69,7 +69,7 @@ size_t rotatek_workspace_bytes(const rotatek_dims* dm, rotatek_op op) {
   if (op == ROTATEK_OP_CALIBRATE)
     return rk::calib_ws_layout(dm->units, dm->head_dim, dm->n_vis, true, nullptr, nullptr);
   if (op == ROTATEK_OP_DECODE)
-    return rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->n_vis, dm->n_text, nullptr,
+    return rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->rank, dm->n_vis, dm->n_text, nullptr,
                                 nullptr);
   return 0;
 }
@@ -155,10 +155,10 @@ rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dm, const void* q, con
   for (const void* p : ptrs)
     if (p && !aligned16(p)) return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
   rk::DecodeWs ws;
-  const size_t need = rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->n_vis, M,
+  const size_t need = rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->rank, dm->n_vis, M,
                                            workspace, &ws);
   if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
-  if (kernel < 0 || kernel > 2) return fail(ROTATEK_ERR_DIMS, "kernel must be 0, 1 or 2");
+  if (kernel < 0 || kernel > 3) return fail(ROTATEK_ERR_DIMS, "kernel must be 0, 1, 2 or 3");
   rk::DecodeArgs a;
   a.U = dm->units; a.G = dm->group; a.d = dm->head_dim; a.r = dm->rank; a.N = dm->n_vis; a.M = M;
   a.bf16 = dm->dtype == ROTATEK_BF16;

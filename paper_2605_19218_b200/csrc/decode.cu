@@ -23,8 +23,12 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cstring>
+#include <type_traits>
+
 #include "common.cuh"
 #include "internal.h"
+#include "tc_common.cuh"
 
 namespace rk {
 
@@ -41,7 +45,55 @@ struct DecodeParams {
   float* out;
   uint32_t* counters;
   float* partials;
+  const float* qt = nullptr;  // [U, G, r] pre-rotated, pre-scaled queries (qrot_kernel)
+  const float* qb = nullptr;  // [U, G] pre-scaled bias
 };
+
+// Programmatic dependent launch: the decode kernel starts while qrot_kernel runs; only the
+// reads of q~ / b wait for it (everything the decode streams was written before qrot).
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+// q~ = q R_r and b = q . dmu for every (unit, query head), pre-scaled by scale*log2(e)
+// (Alg. 2 lines 1-2; App. C P:610-616 inlines this into every program -- here it is computed
+// once per head instead of once per (head, split)).
+template <typename T>
+__global__ void __launch_bounds__(128) qrot_kernel(int G, int d, int r, const T* __restrict__ q,
+                                                   const float* __restrict__ R,
+                                                   const float* __restrict__ dmu, float sl,
+                                                   float* __restrict__ qt, float* __restrict__ qb) {
+  extern __shared__ float qsm[];  // [G][d] q, then [d][r] R_r
+  float* Rs = qsm + G * d;
+  pdl_launch_dependents();
+  const int u = blockIdx.x, tid = threadIdx.x;
+  const T* qu = q + (size_t)u * G * d;
+  const float* Ru = R + (size_t)u * d * r;
+  // stage R_r with independent 16-byte loads (d*r is a multiple of 4 for d % 16 == 0)
+  for (int e = tid; e < d * r / 4; e += blockDim.x)
+    reinterpret_cast<float4*>(Rs)[e] = __ldg(reinterpret_cast<const float4*>(Ru) + e);
+  for (int e = tid; e < G * d; e += blockDim.x) qsm[e] = Elem<T>::to_f(qu[e]);
+  __syncthreads();
+  for (int e = tid; e < G * r; e += blockDim.x) {
+    const int g = e / r, k = e % r;
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll 8
+    for (int i = 0; i < d; i += 2) {
+      s0 = fmaf(qsm[g * d + i], Rs[i * r + k], s0);
+      s1 = fmaf(qsm[g * d + i + 1], Rs[(i + 1) * r + k], s1);
+    }
+    qt[((size_t)u * G + g) * r + k] = (s0 + s1) * sl;
+  }
+  const int w = tid >> 5, lane = tid & 31;
+  for (int g = w; g < G; g += blockDim.x >> 5) {
+    float s = 0.f;
+    if (dmu)
+      for (int i = lane; i < d; i += 32) s = fmaf(qsm[g * d + i], __ldg(dmu + (size_t)u * d + i), s);
+    s = warp_sum(s);
+    if (lane == 0) qb[(size_t)u * G + g] = s * sl;
+  }
+}
 
 // =====================================================================================
 // generic kernel
@@ -169,6 +221,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) decode_generic_kernel(DecodePa
 }
 
 #include "decode_fast.cuh"
+#include "decode_gqa.cuh"
 
 // =====================================================================================
 // host side
@@ -197,6 +250,8 @@ static FastPlan fast_plan(int U, int N, int M, int warps_per_sm) {
   long long nw = (long long)num_sms() * warps_per_sm;
   const long long by_size = (T + 63) / 64;  // at least 64 tokens per warp
   if (by_size < nw) nw = by_size;
+  // at most 126 warps per unit, so a unit's partials (<= 128) fit the merge scratch
+  if (nw > 126LL * U) nw = 126LL * U;
   if (nw < 1) nw = 1;
   pl.NW = (int)nw;
   // a unit spans at most ceil(L / min_range) + 1 warps; min_range >= floor(T/NW)
@@ -217,7 +272,7 @@ int decode_max_splits(int U, int N, int M) {
 
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-size_t decode_ws_layout(int U, int G, int d, int N, int M, void* base, DecodeWs* ws) {
+size_t decode_ws_layout(int U, int G, int d, int r, int N, int M, void* base, DecodeWs* ws) {
   const FastPlan pl = fast_plan(U, N, M, kMaxWarpsPerSM);  // worst case: most warps per unit
   const int smax = 64;  // explicit splits (rotatek_decode_attn_ex) may ask for up to 64
   size_t gen = (size_t)U * G * smax * (d + 2) * 4;
@@ -230,9 +285,47 @@ size_t decode_ws_layout(int U, int G, int d, int N, int M, void* base, DecodeWs*
   off += al256((size_t)U * 4);
   w.partials = (float*)(b ? b + off : nullptr);
   off += al256(part);
+  w.qt = (float*)(b ? b + off : nullptr);
+  off += al256((size_t)U * G * r * 4);
+  w.qb = (float*)(b ? b + off : nullptr);
+  off += al256((size_t)U * G * 4);
   w.max_splits = smax;
   if (ws) *ws = w;
   return off;
+}
+
+static bool launch_qrot(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
+  const size_t sm = ((size_t)a.G * a.d + (size_t)a.d * a.r) * sizeof(float);
+  const float sl = a.scale * kLog2e;
+  static bool attr = [] {
+    cudaFuncSetAttribute(qrot_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    cudaFuncSetAttribute(qrot_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    return true;
+  }();
+  (void)attr;
+  if (a.bf16)
+    qrot_kernel<__nv_bfloat16><<<a.U, 128, sm, st>>>(a.G, a.d, a.r, static_cast<const __nv_bfloat16*>(a.q),
+                                                     a.R, a.dmu, sl, ws.qt, ws.qb);
+  else
+    qrot_kernel<float><<<a.U, 128, sm, st>>>(a.G, a.d, a.r, static_cast<const float*>(a.q), a.R, a.dmu,
+                                             sl, ws.qt, ws.qb);
+  return cudaPeekAtLastError() == cudaSuccess;
+}
+
+// launch `kern` as a programmatic dependent of the preceding qrot_kernel
+template <typename Kern, typename... Args>
+static bool launch_pdl(Kern kern, int ctas, int threads, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...) == cudaSuccess;
 }
 
 template <typename T, int RK, int G, int WARPS, int STAGES, int TTV, int MINB>
@@ -251,9 +344,10 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   const FastPlan pl = fast_plan(a.U, a.N, a.M, ctas_per_sm * WARPS);
   const int ctas = (pl.NW + WARPS - 1) / WARPS;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials};
-  kern<<<ctas, WARPS * 32, C::SMEM, st>>>(p, pl.NW, pl.cmax);
-  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, ws.qt, ws.qb};
+  if (!launch_qrot(a, ws, st)) return -1;
+  if (!launch_pdl(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)) return -1;
+  return 2;
 }
 
 // Default configuration per shape: 16 resident warps per SM (2 CTAs x 8 warps), one
@@ -341,9 +435,63 @@ static bool fast_supported(const DecodeArgs& a) {
   return true;
 }
 
+// ------------------------------------------------------------- tensor-core GQA launcher
+template <int RK, int G>
+constexpr int gqa_warps() {
+  constexpr int per = GqaCfg<RK, G, 1>::WARP_SMEM;
+  constexpr int w = (227 * 1024 - 1024) / per;
+  return w > 8 ? 8 : w;
+}
+
+template <int RK, int G>
+static int launch_gqa_t(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
+  constexpr int WARPS = gqa_warps<RK, G>();
+  using C = GqaCfg<RK, G, WARPS>;
+  GqaMaps maps;
+  memset(&maps, 0, sizeof(maps));
+  if (!encode_tmap_3d_bf16(&maps.kc, a.Kc, RK, a.N, a.U, RK, C::TT, RK * 2)) return -2;
+  if (!encode_tmap_3d_bf16(&maps.v, a.V, kD, a.N, a.U, 64, C::TT, 128)) return -2;
+  if (a.M > 0) {
+    if (!encode_tmap_3d_bf16(&maps.kt, a.Kt, kD, a.M, a.U, 64, C::TX, 128)) return -2;
+    if (!encode_tmap_3d_bf16(&maps.vt, a.Vt, kD, a.M, a.U, 64, C::TX, 128)) return -2;
+  }
+  auto kern = decode_gqa_kernel<RK, G, WARPS>;
+  static bool attr = [&] {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) == cudaSuccess;
+  }();
+  (void)attr;
+  const FastPlan pl = fast_plan(a.U, a.N, a.M, WARPS);
+  const int ctas = (pl.NW + WARPS - 1) / WARPS;
+  DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, ws.qt, ws.qb};
+  if (!launch_qrot(a, ws, st)) return -1;
+  if (!launch_pdl(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, pl.cmax)) return -1;
+  return 2;
+}
+
+template <int RK>
+static int launch_gqa_rk(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
+  switch (a.G) {
+    case 2: return launch_gqa_t<RK, 2>(a, ws, st);
+    case 4: return launch_gqa_t<RK, 4>(a, ws, st);
+    case 7: return launch_gqa_t<RK, 7>(a, ws, st);
+    case 8: return launch_gqa_t<RK, 8>(a, ws, st);
+  }
+  return -2;
+}
+
+static bool gqa_supported(const DecodeArgs& a) {
+  return a.bf16 && a.d == kD && (a.r == 32 || a.r == 64) &&
+         (a.G == 2 || a.G == 4 || a.G == 7 || a.G == 8) && (a.M == 0 || (a.Kt && a.Vt));
+}
+
 int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kernel, cudaStream_t st) {
   const bool fast_ok = fast_supported(a);
-  if (kernel == 2 && !fast_ok) return -2;
+  const bool gqa_ok = gqa_supported(a);
+  if ((kernel == 2 && !fast_ok) || (kernel == 3 && !gqa_ok)) return -2;
+  if (kernel == 3 || (kernel == 0 && gqa_ok && splits <= 0)) {
+    return a.r == 32 ? launch_gqa_rk<32>(a, ws, st) : launch_gqa_rk<64>(a, ws, st);
+  }
   if ((kernel == 0 && fast_ok && splits <= 0) || kernel == 2) {
     return a.bf16 ? launch_fast_rk<__nv_bfloat16>(a, ws, st) : launch_fast_rk<float>(a, ws, st);
   }

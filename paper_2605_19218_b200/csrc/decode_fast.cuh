@@ -119,6 +119,64 @@ __device__ __forceinline__ void load_v4<float>(const unsigned char* p, float* f)
   f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
 }
 
+// Merge the `count` partial records of one unit (acc[kD] | m | l | pad per query head, slot
+// order = range order, so the result is deterministic) and write out[g][:] = acc / l.
+// All G heads and two slots are in flight at once: the merge is latency-bound on L2 reads
+// and sits on the kernel's tail.
+template <int G>
+__device__ __forceinline__ void merge_unit(const float* __restrict__ part, int count,
+                                           float* __restrict__ out, int lane,
+                                           float* __restrict__ wsm /* >= count * G floats */) {
+  constexpr int kRec = kD + 4;
+  // pass 1 (lanes over slots): per-head max of m, then the slot weights 2^(m_s - max) into
+  // shared memory and the merged denominator sum_s l_s 2^(m_s - max)
+  float mloc[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) mloc[g] = -CUDART_INF_F;
+  for (int s = lane; s < count; s += 32)
+#pragma unroll
+    for (int g = 0; g < G; ++g) mloc[g] = fmaxf(mloc[g], __ldcg(part + ((size_t)s * G + g) * kRec + kD));
+  float Ls[G];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    mloc[g] = warp_max(mloc[g]);
+    Ls[g] = 0.f;
+  }
+  for (int s = lane; s < count; s += 32)
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float* src = part + ((size_t)s * G + g) * kRec;
+      const float ms = __ldcg(src + kD);
+      const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - mloc[g]);
+      wsm[s * G + g] = f;
+      Ls[g] = fmaf(__ldcg(src + kD + 1), f, Ls[g]);
+    }
+#pragma unroll
+  for (int g = 0; g < G; ++g) Ls[g] = warp_sum(Ls[g]);
+  __syncwarp();
+  // pass 2 (lanes over channels): weighted sum of the accumulators, 4 slots in flight
+  float A[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g) A[g][0] = A[g][1] = A[g][2] = A[g][3] = 0.f;
+#pragma unroll 4
+  for (int s = 0; s < count; ++s) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(part + ((size_t)s * G + g) * kRec + lane * 4));
+      const float f = wsm[s * G + g];
+      A[g][0] = fmaf(v.x, f, A[g][0]); A[g][1] = fmaf(v.y, f, A[g][1]);
+      A[g][2] = fmaf(v.z, f, A[g][2]); A[g][3] = fmaf(v.w, f, A[g][3]);
+    }
+  }
+  __syncwarp();
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const float inv = 1.f / Ls[g];
+    *reinterpret_cast<float4*>(out + (size_t)g * kD + lane * 4) =
+        make_float4(A[g][0] * inv, A[g][1] * inv, A[g][2] * inv, A[g][3] * inv);
+  }
+}
+
 // One tile: scores (key rows of KR channels), online-softmax rescale, P.V.
 // FULL: tn == TT (branch-free, fully unrolled); else the tail path.
 template <typename T, int KR, int TT, int G, int NACC, bool FULL, bool BIAS>
@@ -286,46 +344,13 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   float qreg[C::CHN], xreg[C::CHN];  // register copies of q~ / q chunks when G == 1
   int cur_u = -1;
 
+  pdl_wait();  // q~ and b come from qrot_kernel (programmatic dependent launch)
   auto setup = [&](int u) {
-    // q (fp32) -> smem; q~ = q R_r and b = q . dmu (Alg. 2 l.1-2); then scale by sl
+    // scaled q (text keys), q~ = q R_r and b = q . dmu precomputed by qrot_kernel
     const T* qg = static_cast<const T*>(p.q) + (size_t)u * G * kD;
-    for (int e = lane; e < G * kD; e += 32) qs[e] = Elem<T>::to_f(qg[e]);
-    __syncwarp();
-    const float* Ru = p.R + (size_t)u * kD * RK;
-    constexpr int KPL = (RK + 31) / 32;
-    float qa[G][KPL];
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) qa[g][j] = 0.f;
-#pragma unroll 4
-    for (int i = 0; i < kD; ++i) {
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) {
-        const int k = lane + 32 * j;
-        const float rv = (k < RK) ? __ldg(Ru + (size_t)i * RK + k) : 0.f;
-#pragma unroll
-        for (int g = 0; g < G; ++g) qa[g][j] = fmaf(qs[g * kD + i], rv, qa[g][j]);
-      }
-    }
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-#pragma unroll
-      for (int j = 0; j < KPL; ++j) {
-        const int k = lane + 32 * j;
-        if (k < RK) qts[g * RK + k] = qa[g][j] * p.sl;
-      }
-      float bb = 0.f;
-      if (p.dmu) {
-#pragma unroll
-        for (int j = 0; j < kD / 32; ++j)
-          bb = fmaf(qs[g * kD + lane + 32 * j], __ldg(p.dmu + (size_t)u * kD + lane + 32 * j), bb);
-      }
-      bb = warp_sum(bb);
-      if (lane == 0) bs[g] = bb * p.sl;
-    }
-    __syncwarp();
-    for (int e = lane; e < G * kD; e += 32) qs[e] *= p.sl;
+    for (int e = lane; e < G * kD; e += 32) qs[e] = Elem<T>::to_f(qg[e]) * p.sl;
+    for (int e = lane; e < G * RK; e += 32) qts[e] = __ldcg(p.qt + (size_t)u * G * RK + e);
+    if (lane < G) bs[lane] = __ldcg(p.qb + (size_t)u * G + lane);
     __syncwarp();
     if constexpr (G == 1) {
       const int cv = lane % C::LPT_V, cx = lane % C::LPT_X;
@@ -387,24 +412,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
     prev = __shfl_sync(0xffffffffu, prev, 0);
     if (prev != (unsigned)(count - 1)) return;
     __threadfence();
-#pragma unroll 1
-    for (int g = 0; g < G; ++g) {
-      float Mx = -CUDART_INF_F;
-      for (int s = 0; s < count; ++s) Mx = fmaxf(Mx, __ldcg(part + ((size_t)s * G + g) * kRec + kD));
-      float Ls = 0.f, R4[4] = {0.f, 0.f, 0.f, 0.f};
-      for (int s = 0; s < count; ++s) {
-        const float* src = part + ((size_t)s * G + g) * kRec;
-        const float ms = __ldcg(src + kD);
-        const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx);
-        Ls = fmaf(__ldcg(src + kD + 1), f, Ls);
-        const float4 v = __ldcg(reinterpret_cast<const float4*>(src + lane * 4));
-        R4[0] = fmaf(v.x, f, R4[0]); R4[1] = fmaf(v.y, f, R4[1]);
-        R4[2] = fmaf(v.z, f, R4[2]); R4[3] = fmaf(v.w, f, R4[3]);
-      }
-      const float inv = 1.f / Ls;
-      *reinterpret_cast<float4*>(p.out + ((size_t)u * G + g) * kD + lane * 4) =
-          make_float4(R4[0] * inv, R4[1] * inv, R4[2] * inv, R4[3] * inv);
-    }
+    merge_unit<G>(part, count, p.out + (size_t)u * G * kD, lane, qs);  // qs is free until setup
     if (lane == 0) p.counters[u] = 0u;
   };
 

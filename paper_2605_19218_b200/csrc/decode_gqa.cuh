@@ -1,0 +1,324 @@
+// decode_gqa.cuh -- tensor-core decode for grouped-query attention (G query heads per KV
+// unit, 2 <= G <= 8; d = 128; r in {32, 64}; bf16 cache).  Included by decode.cu.
+//
+// Same warp-streaming decomposition as decode_fast_kernel (one contiguous token range per
+// warp, per-warp TMA stage, unit-boundary partials merged by the last contributor), but
+// the arithmetic runs on the tensor cores with mma.sync.m16n8k16 (bf16 in, fp32 accumulate):
+//   scores  S[16 x 8] = A[16 x 16] . K~^T   A rows 0..G-1 = q~ rounded to bf16 (hi),
+//                                           rows 8..8+G-1 = q~ - hi rounded (lo); the hi and
+//                                           lo partial scores land in the same thread and are
+//                                           summed, so q~ enters with ~16 significant bits;
+//   P.V     O[16 x 8] = P[16 x 16] . V      P rows 0..7 = bf16(p), rows 8..15 = p - bf16(p);
+// K~ and V tiles are brought by tensor-map TMA (cp.async.bulk.tensor, 64/128-byte swizzle)
+// so that ldmatrix (and ldmatrix.trans for V) reads them without bank conflicts; tokens past
+// the end of a unit are zero-filled by TMA, tokens past the end of the warp's range are masked.
+// tcgen05 is not used here: with M = 2G <= 16 useful rows its 64/128-row tiles would waste
+// 4-8x of the tensor pipe, while the kernel is HBM-bound (~7 flop/byte).
+
+namespace gqa {
+
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+// element x0 -> low 16 bits, x1 -> high 16 bits
+__device__ __forceinline__ uint32_t pack2(float x0, float x1) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(x0, x1);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
+  const float2 hf = __bfloat1622float2(h);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = pack2(x0 - hf.x, x1 - hf.y);
+}
+// byte offset of a 16-byte chunk in a row of a swizzled TMA box (rows of RB bytes)
+template <int RB>
+__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
+  const uint32_t off = row * RB + chunk * 16;
+  if constexpr (RB == 128) return off ^ (((off >> 7) & 7u) << 4);
+  else return off ^ (((off >> 7) & 3u) << 4);  // RB == 64: 64-byte swizzle
+}
+
+}  // namespace gqa
+
+template <int RK, int G, int WARPS>
+struct GqaCfg {
+  static constexpr int TT = 64;                     // visual tile tokens
+  static constexpr int TX = 32;                     // text tile tokens
+  static constexpr int KB = TT * RK * 2;            // K~ box bytes
+  static constexpr int VH = TT * 128;               // one 64-channel V half
+  static constexpr int XH = TX * 128;               // one 64-channel text half
+  static constexpr int STAGE = KB + 2 * VH;         // >= 4 * XH
+  static constexpr int OFF_Q = (STAGE + 1023) / 1024 * 1024;   // float [G][128]
+  static constexpr int OFF_QT = OFF_Q + G * 128 * 4;           // float [G][RK]
+  static constexpr int OFF_B = OFF_QT + G * RK * 4;            // float [8]
+  static constexpr int OFF_BAR = OFF_B + 32;
+  static constexpr int WARP_SMEM = (OFF_BAR + 8 + 1023) / 1024 * 1024;
+  static constexpr int SMEM = WARPS * WARP_SMEM + 1024;        // + alignment slack
+  static_assert(STAGE >= 4 * XH, "text tile must fit the stage");
+  static_assert(RK == 32 || RK == 64, "rank");
+  static_assert(G >= 1 && G <= 8, "group");
+};
+
+struct GqaMaps {
+  CUtensorMap kc, v, kt, vt;
+};
+
+template <int RK, int G, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_constant__ GqaMaps maps,
+                                                                   DecodeParams p, int NW, int cmax) {
+  using C = GqaCfg<RK, G, WARPS>;
+  constexpr int NKS = RK / 16;  // score k-steps
+  extern __shared__ unsigned char gsm_raw[];
+  unsigned char* gsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * WARPS + w;
+  if (gw >= NW) return;
+  unsigned char* base = gsm + w * C::WARP_SMEM;
+  float* qs = reinterpret_cast<float*>(base + C::OFF_Q);
+  float* qts = reinterpret_cast<float*>(base + C::OFF_QT);
+  float* bs = reinterpret_cast<float*>(base + C::OFF_B);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
+  const uint32_t sbase = smem_u32(base);
+
+  const int N = p.N, M = p.M;
+  const long long L = (long long)N + M;
+  const long long Ttot = L * p.U;
+  const long long a = range_start(Ttot, gw, NW), b = range_start(Ttot, gw + 1, NW);
+  if (a >= b) return;
+  const uint64_t pol = policy_evict_first();
+  if (lane == 0) {
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    tc::prefetch_tmap(&maps.kc);
+    tc::prefetch_tmap(&maps.v);
+    if (M > 0) {
+      tc::prefetch_tmap(&maps.kt);
+      tc::prefetch_tmap(&maps.vt);
+    }
+  }
+  __syncwarp();
+
+  long long px = a;
+  auto issue = [&]() {
+    const Tile tl = tile_at<C::TT, C::TX>(px, b, N, M);
+    if (tl.vis) {
+      mbar_arrive_expect_tx(bar, C::KB + 2 * C::VH);
+      tc::tma_load_3d(base, &maps.kc, 0, tl.t, tl.u, bar, pol);
+      tc::tma_load_3d(base + C::KB, &maps.v, 0, tl.t, tl.u, bar, pol);
+      tc::tma_load_3d(base + C::KB + C::VH, &maps.v, 64, tl.t, tl.u, bar, pol);
+    } else {
+      mbar_arrive_expect_tx(bar, 4 * C::XH);
+      tc::tma_load_3d(base, &maps.kt, 0, tl.t, tl.u, bar, pol);
+      tc::tma_load_3d(base + C::XH, &maps.kt, 64, tl.t, tl.u, bar, pol);
+      tc::tma_load_3d(base + 2 * C::XH, &maps.vt, 0, tl.t, tl.u, bar, pol);
+      tc::tma_load_3d(base + 3 * C::XH, &maps.vt, 64, tl.t, tl.u, bar, pol);
+    }
+    px += tl.tn;
+  };
+  if (lane == 0) issue();
+
+  const int g = lane >> 2, c = lane & 3;
+  const bool live = g < G;
+  uint32_t aq[NKS][4];   // q~ hi/lo A fragments
+  uint32_t ax[8][4];     // q hi/lo A fragments (text)
+  float bg = 0.f;
+  float m = -CUDART_INF_F, l = 0.f;
+  float acc[16][4];
+  int cur_u = -1;
+
+  pdl_wait();  // q~ and b come from qrot_kernel (programmatic dependent launch)
+  auto setup = [&](int u) {
+    const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(p.q) + (size_t)u * G * kD;
+    for (int e = lane; e < G * kD; e += 32) qs[e] = __bfloat162float(qg[e]);
+    for (int e = lane; e < G * RK; e += 32) qts[e] = __ldcg(p.qt + (size_t)u * G * RK + e);
+    if (lane < G) bs[lane] = __ldcg(p.qb + (size_t)u * G + lane);
+    __syncwarp();
+    // A fragments: row g (hi) / g + 8 (lo); k columns 2c, 2c+1 (low half) and 8 + 2c, 9 + 2c
+#pragma unroll
+    for (int kk = 0; kk < NKS; ++kk) {
+      const int k0 = 16 * kk + 2 * c;
+      float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+      if (live) {
+        x0 = qts[g * RK + k0]; x1 = qts[g * RK + k0 + 1];
+        y0 = qts[g * RK + k0 + 8]; y1 = qts[g * RK + k0 + 9];
+      }
+      gqa::split2(x0, x1, aq[kk][0], aq[kk][1]);
+      gqa::split2(y0, y1, aq[kk][2], aq[kk][3]);
+    }
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const int k0 = 16 * kk + 2 * c;
+      float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
+      if (live) {
+        x0 = qs[g * kD + k0] * p.sl; x1 = qs[g * kD + k0 + 1] * p.sl;
+        y0 = qs[g * kD + k0 + 8] * p.sl; y1 = qs[g * kD + k0 + 9] * p.sl;
+      }
+      gqa::split2(x0, x1, ax[kk][0], ax[kk][1]);
+      gqa::split2(y0, y1, ax[kk][2], ax[kk][3]);
+    }
+    bg = live ? bs[g] : 0.f;
+    __syncwarp();
+    m = -CUDART_INF_F;
+    l = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][e] = 0.f;
+  };
+
+  // online softmax over NB n-blocks of scores s[NB][2] (row g), then P.V from V halves
+  auto softmax_pv = [&](auto nb_tag, float (&s)[decltype(nb_tag)::value][2], uint32_t v0, uint32_t vhalf) {
+    constexpr int NB = decltype(nb_tag)::value;
+    float tmax = -CUDART_INF_F;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) tmax = fmaxf(tmax, fmaxf(s[j][0], s[j][1]));
+    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+    const float mn = live ? fmaxf(m, tmax) : 0.f;
+    const float alpha = live ? fast_exp2(m - mn) : 0.f;
+    m = mn;
+    l *= alpha;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][e] *= alpha;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      s[j][0] = live ? fast_exp2(s[j][0] - mn) : 0.f;
+      s[j][1] = live ? fast_exp2(s[j][1] - mn) : 0.f;
+      l += s[j][0] + s[j][1];
+    }
+#pragma unroll
+    for (int kt = 0; kt < NB / 2; ++kt) {
+      uint32_t pa[4];
+      gqa::split2(s[2 * kt][0], s[2 * kt][1], pa[0], pa[1]);
+      gqa::split2(s[2 * kt + 1][0], s[2 * kt + 1][1], pa[2], pa[3]);
+      const int mid = lane >> 3, r8 = lane & 7;
+      const uint32_t tok = 16 * kt + r8 + 8 * (mid & 1);
+#pragma unroll
+      for (int cbp = 0; cbp < 8; ++cbp) {
+        const uint32_t cb = 2 * cbp + (mid >> 1);
+        const uint32_t addr = v0 + (cb >> 3) * vhalf + gqa::swz<128>(tok, cb & 7);
+        uint32_t b0, b1, b2, b3;
+        gqa::ldsm_x4_t(addr, b0, b1, b2, b3);
+        gqa::mma16816(acc[2 * cbp], pa, b0, b1);
+        gqa::mma16816(acc[2 * cbp + 1], pa, b2, b3);
+      }
+    }
+  };
+
+  auto flush = [&](int u) {
+    const long long x0 = (long long)u * L, x1 = x0 + L - 1;
+    const int first = warp_of(x0, Ttot, NW), last = warp_of(x1, Ttot, NW);
+    const int count = last - first + 1;
+    float lt = l + __shfl_xor_sync(0xffffffffu, l, 1);
+    lt += __shfl_xor_sync(0xffffffffu, lt, 2);
+    constexpr int kRec = kD + 4;
+    if (count == 1) {
+      if (live) {
+        const float inv = 1.f / lt;
+        float* o = p.out + ((size_t)u * G + g) * kD + 2 * c;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          *reinterpret_cast<float2*>(o + 8 * j) =
+              make_float2((acc[j][0] + acc[j][2]) * inv, (acc[j][1] + acc[j][3]) * inv);
+      }
+      return;
+    }
+    const int slot = gw - first;
+    float* part = p.partials + ((size_t)u * cmax) * G * kRec;
+    if (live) {
+      float* dst = part + ((size_t)slot * G + g) * kRec;
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        *reinterpret_cast<float2*>(dst + 8 * j + 2 * c) = make_float2(acc[j][0] + acc[j][2], acc[j][1] + acc[j][3]);
+      if (c == 0) { dst[kD] = m; dst[kD + 1] = lt; }
+    }
+    __threadfence();
+    __syncwarp();
+    unsigned prev = 0;
+    if (lane == 0) prev = atomicAdd(&p.counters[u], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != (unsigned)(count - 1)) return;
+    __threadfence();
+    merge_unit<G>(part, count, p.out + (size_t)u * G * kD, lane, qs);  // qs is free until setup
+    if (lane == 0) p.counters[u] = 0u;
+  };
+
+  using NbV = std::integral_constant<int, C::TT / 8>;
+  using NbX = std::integral_constant<int, C::TX / 8>;
+
+  long long cx = a;
+  int j = 0;
+  while (cx < b) {
+    const Tile tl = tile_at<C::TT, C::TX>(cx, b, N, M);
+    if (tl.u != cur_u) {
+      if (cur_u >= 0) flush(cur_u);
+      setup(tl.u);
+      cur_u = tl.u;
+    }
+    mbar_wait(bar, (uint32_t)(j & 1));
+    const int mid = lane >> 3, r8 = lane & 7;
+    if (tl.vis) {
+      float s[NbV::value][2];
+#pragma unroll
+      for (int nb = 0; nb < NbV::value; ++nb) {
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t row = 8 * nb + r8;
+#pragma unroll
+        for (int kp = 0; kp < RK / 32; ++kp) {
+          uint32_t b0, b1, b2, b3;
+          gqa::ldsm_x4(sbase + gqa::swz<RK * 2>(row, 4 * kp + mid), b0, b1, b2, b3);
+          gqa::mma16816(d, aq[2 * kp], b0, b1);
+          gqa::mma16816(d, aq[2 * kp + 1], b2, b3);
+        }
+        const int t0 = 8 * nb + 2 * c;
+        s[nb][0] = (t0 < tl.tn) ? d[0] + d[2] + bg : -CUDART_INF_F;
+        s[nb][1] = (t0 + 1 < tl.tn) ? d[1] + d[3] + bg : -CUDART_INF_F;
+      }
+      softmax_pv(NbV{}, s, sbase + C::KB, C::VH);
+    } else {
+      float s[NbX::value][2];
+#pragma unroll
+      for (int nb = 0; nb < NbX::value; ++nb) {
+        float d[4] = {0.f, 0.f, 0.f, 0.f};
+        const uint32_t row = 8 * nb + r8;
+#pragma unroll
+        for (int kp = 0; kp < 4; ++kp) {
+          const uint32_t ch = 4 * kp + mid;  // 16-byte chunk 0..15 of the 256-byte row
+          uint32_t b0, b1, b2, b3;
+          gqa::ldsm_x4(sbase + (ch >> 3) * C::XH + gqa::swz<128>(row, ch & 7), b0, b1, b2, b3);
+          gqa::mma16816(d, ax[2 * kp], b0, b1);
+          gqa::mma16816(d, ax[2 * kp + 1], b2, b3);
+        }
+        const int t0 = 8 * nb + 2 * c;
+        s[nb][0] = (t0 < tl.tn) ? d[0] + d[2] : -CUDART_INF_F;
+        s[nb][1] = (t0 + 1 < tl.tn) ? d[1] + d[3] : -CUDART_INF_F;
+      }
+      softmax_pv(NbX{}, s, sbase + 2 * C::XH, C::XH);
+    }
+    __syncwarp();
+    if (lane == 0 && px < b) {
+      fence_proxy_async();
+      issue();
+    }
+    cx += tl.tn;
+    ++j;
+  }
+  if (cur_u >= 0) flush(cur_u);
+}

@@ -23,14 +23,16 @@ struct CalibWs {
 
 struct DecodeWs {
   uint32_t* counters;  // [U] zero on entry, left zero
-  float* partials;     // [U, G, S, d + 2]
+  float* partials;     // [U, G, S, d + 2] (generic) or [U, cmax, G, d + 4] (streaming)
+  float* qt;           // [U, G, r]  q~ = q R_r * scale * log2(e)   (written by qrot_kernel)
+  float* qb;           // [U, G]     b  = q . dmu * scale * log2(e)
   int max_splits;
 };
 
 int cov_parts(int U, int N);
 int decode_max_splits(int U, int N, int M);
 size_t calib_ws_layout(int U, int d, int N, bool fp64_eig, void* base, CalibWs* ws);
-size_t decode_ws_layout(int U, int G, int d, int N, int M, void* base, DecodeWs* ws);
+size_t decode_ws_layout(int U, int G, int d, int r, int N, int M, void* base, DecodeWs* ws);
 
 // each returns the number of launches enqueued (>= 0) or -1 on launch error
 int launch_sigma(int U, int G, int W, int d, bool bf16, bool weight, const void* Qw,

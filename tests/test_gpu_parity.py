@@ -82,6 +82,32 @@ def test_decode_on_oracle_cache(rk, name, dtype, kernel):
     assert err <= TOL[dtype], (name, dtype, kernel, err)
 
 
+@pytest.mark.parametrize("group,rank,h_kv,n_vis,n_text", [(7, 32, 2, 517, 21), (7, 64, 2, 300, 0),
+                                                          (2, 32, 3, 130, 5), (4, 64, 1, 64, 64),
+                                                          (8, 32, 2, 1000, 33), (7, 32, 40, 61, 3)])
+@pytest.mark.parametrize("kernel", [3, 2])
+def test_decode_gqa_kernels(rk, group, rank, h_kv, n_vis, n_text, kernel):
+    """Tensor-core GQA decode (mma.sync, hi/lo split q~ and P, TMA tensor maps) and the
+    CUDA-core streaming kernel against the oracle on the same cache bytes."""
+    import torch
+    if kernel == 2 and group not in (1, 7):
+        pytest.skip("CUDA-core streaming kernel is instantiated for G in {1, 7}")
+    cfg = CONFIGS["qwen_b1_r32"].with_(group=group, rank=rank, h_kv=h_kv, n_vis=n_vis, n_text=n_text)
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, "bf16")
+    M = cfg.n_text
+    ref = orc.decode(w["q"].f64(), Kt, w["V"].f64(), R, dmu,
+                     w["Ktext"].f64() if M else None, w["Vtext"].f64() if M else None)
+    out = rk.decode_attn(to_torch(w["q"]), _as_dev(Kt, "bf16"), to_torch(w["V"]),
+                         torch.from_numpy(R.astype(np.float32)).cuda(),
+                         torch.from_numpy(dmu.astype(np.float32)).cuda(),
+                         to_torch(w["Ktext"]) if M else None, to_torch(w["Vtext"]) if M else None,
+                         kernel=kernel)
+    torch.cuda.synchronize()
+    err = max_rel_err(to_np64(out), ref)
+    assert err <= 1e-3, err
+
+
 @pytest.mark.parametrize("splits", [1, 2, 3, 7, 64])
 def test_decode_split_invariance(rk, splits):
     """Split-K over the token axis is an exact re-association (App. C)."""
