@@ -44,6 +44,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="llava_b32")
+    ap.add_argument("--override", default="",
+                    help="experiments only: comma list of Config fields, e.g. group=2,batch=8")
     ap.add_argument("--layers", type=int, default=4)
     ap.add_argument("--kernel", type=int, default=0, help="0 auto, 1 generic, 2 fast")
     ap.add_argument("--no-graph", action="store_true")
@@ -67,6 +69,17 @@ def peaks():
         d = json.load(open(p))
         return d["hbm_gbs"], "measured", d
     return 6650.0, "fallback (B200_PROFILING.md)", {}
+
+
+def get_config(args):
+    cfg = CONFIGS[args.config]
+    if args.override:
+        kw = {}
+        for item in args.override.split(","):
+            k, v = item.split("=")
+            kw[k] = type(getattr(cfg, k))(v)
+        cfg = cfg.with_(**kw)
+    return cfg
 
 
 def rank_units(cfg, rank):
@@ -105,7 +118,7 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    cfg = CONFIGS[args.config]
+    cfg = get_config(args)
     from oracle import oracle as orc
     n_units = max(1, min(cfg.units, 32))
     w = make_workload(cfg, units=range(n_units), threads=os.cpu_count() or 8)
@@ -209,7 +222,7 @@ def run_ours(args):
         dist.init_process_group("nccl")
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    cfg = CONFIGS[args.config]
+    cfg = get_config(args)
     L = args.layers
     peak_gbs, peak_kind, _ = peaks()
 

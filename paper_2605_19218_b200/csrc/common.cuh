@@ -56,6 +56,14 @@ __device__ __forceinline__ float warp_max(float v) {
   return v;
 }
 
+// ticket for the last-arriver merge: release (cumulative, so the warp's partial stores
+// ordered before it by __syncwarp are published) + acquire for the merging warp
+__device__ __forceinline__ unsigned atom_add_acq_rel_gpu(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 __device__ __forceinline__ float fast_exp2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

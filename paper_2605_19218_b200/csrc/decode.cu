@@ -64,16 +64,18 @@ __global__ void __launch_bounds__(128) qrot_kernel(int G, int d, int r, const T*
                                                    const float* __restrict__ R,
                                                    const float* __restrict__ dmu, float sl,
                                                    float* __restrict__ qt, float* __restrict__ qb) {
-  extern __shared__ float qsm[];  // [G][d] q, then [d][r] R_r
-  float* Rs = qsm + G * d;
+  extern __shared__ float qsm[];  // [G][d] q, [d] dmu, then [d][r] R_r
+  float* dms = qsm + G * d;
+  float* Rs = dms + d;
   pdl_launch_dependents();
   const int u = blockIdx.x, tid = threadIdx.x;
   const T* qu = q + (size_t)u * G * d;
   const float* Ru = R + (size_t)u * d * r;
-  // stage R_r with independent 16-byte loads (d*r is a multiple of 4 for d % 16 == 0)
+  // one round trip: R_r (independent 16-byte loads; d*r is a multiple of 4), q and dmu
   for (int e = tid; e < d * r / 4; e += blockDim.x)
     reinterpret_cast<float4*>(Rs)[e] = __ldg(reinterpret_cast<const float4*>(Ru) + e);
   for (int e = tid; e < G * d; e += blockDim.x) qsm[e] = Elem<T>::to_f(qu[e]);
+  for (int e = tid; e < d; e += blockDim.x) dms[e] = dmu ? __ldg(dmu + (size_t)u * d + e) : 0.f;
   __syncthreads();
   for (int e = tid; e < G * r; e += blockDim.x) {
     const int g = e / r, k = e % r;
@@ -88,8 +90,7 @@ __global__ void __launch_bounds__(128) qrot_kernel(int G, int d, int r, const T*
   const int w = tid >> 5, lane = tid & 31;
   for (int g = w; g < G; g += blockDim.x >> 5) {
     float s = 0.f;
-    if (dmu)
-      for (int i = lane; i < d; i += 32) s = fmaf(qsm[g * d + i], __ldg(dmu + (size_t)u * d + i), s);
+    for (int i = lane; i < d; i += 32) s = fmaf(qsm[g * d + i], dms[i], s);
     s = warp_sum(s);
     if (lane == 0) qb[(size_t)u * G + g] = s * sl;
   }
@@ -295,7 +296,7 @@ size_t decode_ws_layout(int U, int G, int d, int r, int N, int M, void* base, De
 }
 
 static bool launch_qrot(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
-  const size_t sm = ((size_t)a.G * a.d + (size_t)a.d * a.r) * sizeof(float);
+  const size_t sm = ((size_t)a.G * a.d + a.d + (size_t)a.d * a.r) * sizeof(float);
   const float sl = a.scale * kLog2e;
   static bool attr = [] {
     cudaFuncSetAttribute(qrot_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
@@ -436,17 +437,17 @@ static bool fast_supported(const DecodeArgs& a) {
 }
 
 // ------------------------------------------------------------- tensor-core GQA launcher
-template <int RK, int G>
+template <int RK, int G, int TTV, int STAGES, int MAXW>
 constexpr int gqa_warps() {
-  constexpr int per = GqaCfg<RK, G, 1>::WARP_SMEM;
+  constexpr int per = GqaCfg<RK, G, 1, TTV, STAGES>::WARP_SMEM;
   constexpr int w = (227 * 1024 - 1024) / per;
-  return w > 8 ? 8 : w;
+  return w > MAXW ? MAXW : w;
 }
 
-template <int RK, int G>
-static int launch_gqa_t(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
-  constexpr int WARPS = gqa_warps<RK, G>();
-  using C = GqaCfg<RK, G, WARPS>;
+template <int RK, int G, int TTV, int STAGES, int MAXW = 8>
+static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
+  constexpr int WARPS = gqa_warps<RK, G, TTV, STAGES, MAXW>();
+  using C = GqaCfg<RK, G, WARPS, TTV, STAGES>;
   GqaMaps maps;
   memset(&maps, 0, sizeof(maps));
   if (!encode_tmap_3d_bf16(&maps.kc, a.Kc, RK, a.N, a.U, RK, C::TT, RK * 2)) return -2;
@@ -455,7 +456,7 @@ static int launch_gqa_t(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st
     if (!encode_tmap_3d_bf16(&maps.kt, a.Kt, kD, a.M, a.U, 64, C::TX, 128)) return -2;
     if (!encode_tmap_3d_bf16(&maps.vt, a.Vt, kD, a.M, a.U, 64, C::TX, 128)) return -2;
   }
-  auto kern = decode_gqa_kernel<RK, G, WARPS>;
+  auto kern = decode_gqa_kernel<RK, G, WARPS, TTV, STAGES>;
   static bool attr = [&] {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) == cudaSuccess;
   }();
@@ -467,6 +468,27 @@ static int launch_gqa_t(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st
   if (!launch_qrot(a, ws, st)) return -1;
   if (!launch_pdl(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, pl.cmax)) return -1;
   return 2;
+}
+
+// ring configuration (ROTATEK_GQA_CFG="tile,stages" for tuning; default one 64-token stage
+// per warp, 8 warps per SM -- the sweep in profiles/ found deeper rings with smaller tiles
+// no faster: the remaining gap on small-U shapes is fixed per-launch latency, not bytes
+// in flight)
+template <int RK, int G>
+static int launch_gqa_t(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
+  static int cfg = [] {
+    const char* e = getenv("ROTATEK_GQA_CFG");
+    int t = 0, s = 0;
+    if (e && sscanf(e, "%d,%d", &t, &s) == 2) return t * 10 + s;
+    return 0;
+  }();
+  switch (cfg) {
+    case 641: return launch_gqa_cfg<RK, G, 64, 1>(a, ws, st);
+    case 322: return launch_gqa_cfg<RK, G, 32, 2>(a, ws, st);
+    case 323: return launch_gqa_cfg<RK, G, 32, 3>(a, ws, st);
+    case 642: return launch_gqa_cfg<RK, G, 64, 2>(a, ws, st);
+    default: return launch_gqa_cfg<RK, G, 64, 1>(a, ws, st);
+  }
 }
 
 template <int RK>

@@ -348,17 +348,29 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   auto setup = [&](int u) {
     // scaled q (text keys), q~ = q R_r and b = q . dmu precomputed by qrot_kernel
     const T* qg = static_cast<const T*>(p.q) + (size_t)u * G * kD;
-    for (int e = lane; e < G * kD; e += 32) qs[e] = Elem<T>::to_f(qg[e]) * p.sl;
-    for (int e = lane; e < G * RK; e += 32) qts[e] = __ldcg(p.qt + (size_t)u * G * RK + e);
-    if (lane < G) bs[lane] = __ldcg(p.qb + (size_t)u * G + lane);
-    __syncwarp();
     if constexpr (G == 1) {
+      // register chunks straight from global memory (independent 16-byte loads)
       const int cv = lane % C::LPT_V, cx = lane % C::LPT_X;
+      const float4* t4 = reinterpret_cast<const float4*>(p.qt + (size_t)u * RK + cv * C::CHN);
+      float4 tv[C::CHN / 4];
 #pragma unroll
-      for (int i = 0; i < C::CHN; ++i) {
-        qreg[i] = qts[cv * C::CHN + i];
-        xreg[i] = qs[cx * C::CHN + i];
+      for (int i = 0; i < C::CHN / 4; ++i) tv[i] = __ldcg(t4 + i);
+      float xf[C::CHN];
+      unpack_chunk<T>(reinterpret_cast<const unsigned char*>(qg + cx * C::CHN), xf);
+      const float bq = __ldcg(p.qb + u);
+#pragma unroll
+      for (int i = 0; i < C::CHN / 4; ++i) {
+        qreg[4 * i] = tv[i].x; qreg[4 * i + 1] = tv[i].y; qreg[4 * i + 2] = tv[i].z; qreg[4 * i + 3] = tv[i].w;
       }
+#pragma unroll
+      for (int i = 0; i < C::CHN; ++i) xreg[i] = xf[i] * p.sl;
+      if (lane == 0) bs[0] = bq;
+      __syncwarp();
+    } else {
+      for (int e = lane; e < G * kD; e += 32) qs[e] = Elem<T>::to_f(qg[e]) * p.sl;
+      for (int e = lane; e < G * RK; e += 32) qts[e] = __ldcg(p.qt + (size_t)u * G * RK + e);
+      if (lane < G) bs[lane] = __ldcg(p.qb + (size_t)u * G + lane);
+      __syncwarp();
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
@@ -405,13 +417,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
       if (lane == 0) { dst[kD] = m[g]; dst[kD + 1] = lt[g]; }
       *reinterpret_cast<float4*>(dst + lane * 4) = make_float4(A[g][0], A[g][1], A[g][2], A[g][3]);
     }
-    __threadfence();
     __syncwarp();
     unsigned prev = 0;
-    if (lane == 0) prev = atomicAdd(&p.counters[u], 1u);
+    if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], 1u);
     prev = __shfl_sync(0xffffffffu, prev, 0);
     if (prev != (unsigned)(count - 1)) return;
-    __threadfence();
     merge_unit<G>(part, count, p.out + (size_t)u * G * kD, lane, qs);  // qs is free until setup
     if (lane == 0) p.counters[u] = 0u;
   };

@@ -55,21 +55,23 @@ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
 
 }  // namespace gqa
 
-template <int RK, int G, int WARPS>
+template <int RK, int G, int WARPS, int TTV = 64, int STAGES = 1>
 struct GqaCfg {
-  static constexpr int TT = 64;                     // visual tile tokens
-  static constexpr int TX = 32;                     // text tile tokens
+  static constexpr int TT = TTV;                    // visual tile tokens
   static constexpr int KB = TT * RK * 2;            // K~ box bytes
   static constexpr int VH = TT * 128;               // one 64-channel V half
+  static constexpr int STAGE = (KB + 2 * VH + 1023) / 1024 * 1024;
+  static constexpr int TX = (STAGE / 512) / 16 * 16;  // text tile tokens (4 halves fit a stage)
   static constexpr int XH = TX * 128;               // one 64-channel text half
-  static constexpr int STAGE = KB + 2 * VH;         // >= 4 * XH
-  static constexpr int OFF_Q = (STAGE + 1023) / 1024 * 1024;   // float [G][128]
+  static constexpr int NSTG = STAGES;
+  static constexpr int OFF_Q = NSTG * STAGE;                   // float [G][128] (merge scratch)
   static constexpr int OFF_QT = OFF_Q + G * 128 * 4;           // float [G][RK]
   static constexpr int OFF_B = OFF_QT + G * RK * 4;            // float [8]
   static constexpr int OFF_BAR = OFF_B + 32;
-  static constexpr int WARP_SMEM = (OFF_BAR + 8 + 1023) / 1024 * 1024;
+  static constexpr int WARP_SMEM = (OFF_BAR + 8 * NSTG + 1023) / 1024 * 1024;
   static constexpr int SMEM = WARPS * WARP_SMEM + 1024;        // + alignment slack
-  static_assert(STAGE >= 4 * XH, "text tile must fit the stage");
+  static_assert(STAGE >= 4 * XH && TX >= 16, "text tile must fit the stage");
+  static_assert(TT % 16 == 0 && KB % 1024 == 0, "tile");
   static_assert(RK == 32 || RK == 64, "rank");
   static_assert(G >= 1 && G <= 8, "group");
 };
@@ -78,10 +80,10 @@ struct GqaMaps {
   CUtensorMap kc, v, kt, vt;
 };
 
-template <int RK, int G, int WARPS>
+template <int RK, int G, int WARPS, int TTV, int STAGES>
 __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_constant__ GqaMaps maps,
                                                                    DecodeParams p, int NW, int cmax) {
-  using C = GqaCfg<RK, G, WARPS>;
+  using C = GqaCfg<RK, G, WARPS, TTV, STAGES>;
   constexpr int NKS = RK / 16;  // score k-steps
   extern __shared__ unsigned char gsm_raw[];
   unsigned char* gsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
@@ -102,7 +104,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   if (a >= b) return;
   const uint64_t pol = policy_evict_first();
   if (lane == 0) {
-    mbar_init(bar, 1);
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
     tc::prefetch_tmap(&maps.kc);
     tc::prefetch_tmap(&maps.v);
@@ -114,23 +116,26 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   __syncwarp();
 
   long long px = a;
-  auto issue = [&]() {
+  auto issue = [&](int st) {
     const Tile tl = tile_at<C::TT, C::TX>(px, b, N, M);
+    unsigned char* dst = base + st * C::STAGE;
+    uint64_t* bb = &bar[st];
     if (tl.vis) {
-      mbar_arrive_expect_tx(bar, C::KB + 2 * C::VH);
-      tc::tma_load_3d(base, &maps.kc, 0, tl.t, tl.u, bar, pol);
-      tc::tma_load_3d(base + C::KB, &maps.v, 0, tl.t, tl.u, bar, pol);
-      tc::tma_load_3d(base + C::KB + C::VH, &maps.v, 64, tl.t, tl.u, bar, pol);
+      mbar_arrive_expect_tx(bb, C::KB + 2 * C::VH);
+      tc::tma_load_3d(dst, &maps.kc, 0, tl.t, tl.u, bb, pol);
+      tc::tma_load_3d(dst + C::KB, &maps.v, 0, tl.t, tl.u, bb, pol);
+      tc::tma_load_3d(dst + C::KB + C::VH, &maps.v, 64, tl.t, tl.u, bb, pol);
     } else {
-      mbar_arrive_expect_tx(bar, 4 * C::XH);
-      tc::tma_load_3d(base, &maps.kt, 0, tl.t, tl.u, bar, pol);
-      tc::tma_load_3d(base + C::XH, &maps.kt, 64, tl.t, tl.u, bar, pol);
-      tc::tma_load_3d(base + 2 * C::XH, &maps.vt, 0, tl.t, tl.u, bar, pol);
-      tc::tma_load_3d(base + 3 * C::XH, &maps.vt, 64, tl.t, tl.u, bar, pol);
+      mbar_arrive_expect_tx(bb, 4 * C::XH);
+      tc::tma_load_3d(dst, &maps.kt, 0, tl.t, tl.u, bb, pol);
+      tc::tma_load_3d(dst + C::XH, &maps.kt, 64, tl.t, tl.u, bb, pol);
+      tc::tma_load_3d(dst + 2 * C::XH, &maps.vt, 0, tl.t, tl.u, bb, pol);
+      tc::tma_load_3d(dst + 3 * C::XH, &maps.vt, 64, tl.t, tl.u, bb, pol);
     }
     px += tl.tn;
   };
-  if (lane == 0) issue();
+  if (lane == 0)
+    for (int s = 0; s < STAGES && px < b; ++s) issue(s);
 
   const int g = lane >> 2, c = lane & 3;
   const bool live = g < G;
@@ -143,36 +148,39 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
 
   pdl_wait();  // q~ and b come from qrot_kernel (programmatic dependent launch)
   auto setup = [&](int u) {
-    const __nv_bfloat16* qg = static_cast<const __nv_bfloat16*>(p.q) + (size_t)u * G * kD;
-    for (int e = lane; e < G * kD; e += 32) qs[e] = __bfloat162float(qg[e]);
-    for (int e = lane; e < G * RK; e += 32) qts[e] = __ldcg(p.qt + (size_t)u * G * RK + e);
-    if (lane < G) bs[lane] = __ldcg(p.qb + (size_t)u * G + lane);
-    __syncwarp();
-    // A fragments: row g (hi) / g + 8 (lo); k columns 2c, 2c+1 (low half) and 8 + 2c, 9 + 2c
+    // A fragments straight from global memory (all loads independent): row g holds the
+    // bf16 "hi" part, row g + 8 the "lo" remainder; k columns 2c, 2c+1 and 8+2c, 9+2c.
+    const int gl = live ? g : 0;
+    const float2* t2 = reinterpret_cast<const float2*>(p.qt + ((size_t)u * G + gl) * RK);
+    const __nv_bfloat162* q2 =
+        reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(p.q) + ((size_t)u * G + gl) * kD);
+    float2 tq[NKS][2];
+    __nv_bfloat162 xq[8][2];
 #pragma unroll
     for (int kk = 0; kk < NKS; ++kk) {
-      const int k0 = 16 * kk + 2 * c;
-      float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
-      if (live) {
-        x0 = qts[g * RK + k0]; x1 = qts[g * RK + k0 + 1];
-        y0 = qts[g * RK + k0 + 8]; y1 = qts[g * RK + k0 + 9];
-      }
-      gqa::split2(x0, x1, aq[kk][0], aq[kk][1]);
-      gqa::split2(y0, y1, aq[kk][2], aq[kk][3]);
+      tq[kk][0] = __ldcg(t2 + 8 * kk + c);
+      tq[kk][1] = __ldcg(t2 + 8 * kk + 4 + c);
     }
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
-      const int k0 = 16 * kk + 2 * c;
-      float x0 = 0.f, x1 = 0.f, y0 = 0.f, y1 = 0.f;
-      if (live) {
-        x0 = qs[g * kD + k0] * p.sl; x1 = qs[g * kD + k0 + 1] * p.sl;
-        y0 = qs[g * kD + k0 + 8] * p.sl; y1 = qs[g * kD + k0 + 9] * p.sl;
-      }
-      gqa::split2(x0, x1, ax[kk][0], ax[kk][1]);
-      gqa::split2(y0, y1, ax[kk][2], ax[kk][3]);
+      xq[kk][0] = q2[8 * kk + c];
+      xq[kk][1] = q2[8 * kk + 4 + c];
     }
-    bg = live ? bs[g] : 0.f;
-    __syncwarp();
+    const float bq = __ldcg(p.qb + (size_t)u * G + gl);
+    const float z = live ? 1.f : 0.f;
+#pragma unroll
+    for (int kk = 0; kk < NKS; ++kk) {
+      gqa::split2(z * tq[kk][0].x, z * tq[kk][0].y, aq[kk][0], aq[kk][1]);
+      gqa::split2(z * tq[kk][1].x, z * tq[kk][1].y, aq[kk][2], aq[kk][3]);
+    }
+    const float zs = z * p.sl;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {
+      const float2 lo = __bfloat1622float2(xq[kk][0]), hi = __bfloat1622float2(xq[kk][1]);
+      gqa::split2(zs * lo.x, zs * lo.y, ax[kk][0], ax[kk][1]);
+      gqa::split2(zs * hi.x, zs * hi.y, ax[kk][2], ax[kk][3]);
+    }
+    bg = z * bq;
     m = -CUDART_INF_F;
     l = 0.f;
 #pragma unroll
@@ -249,13 +257,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
         *reinterpret_cast<float2*>(dst + 8 * j + 2 * c) = make_float2(acc[j][0] + acc[j][2], acc[j][1] + acc[j][3]);
       if (c == 0) { dst[kD] = m; dst[kD + 1] = lt; }
     }
-    __threadfence();
     __syncwarp();
     unsigned prev = 0;
-    if (lane == 0) prev = atomicAdd(&p.counters[u], 1u);
+    if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], 1u);
     prev = __shfl_sync(0xffffffffu, prev, 0);
     if (prev != (unsigned)(count - 1)) return;
-    __threadfence();
     merge_unit<G>(part, count, p.out + (size_t)u * G * kD, lane, qs);  // qs is free until setup
     if (lane == 0) p.counters[u] = 0u;
   };
@@ -272,7 +278,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
       setup(tl.u);
       cur_u = tl.u;
     }
-    mbar_wait(bar, (uint32_t)(j & 1));
+    const int st = j % STAGES;
+    mbar_wait(&bar[st], (uint32_t)((j / STAGES) & 1));
+    const uint32_t sb = sbase + st * C::STAGE;
     const int mid = lane >> 3, r8 = lane & 7;
     if (tl.vis) {
       float s[NbV::value][2];
@@ -283,7 +291,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
 #pragma unroll
         for (int kp = 0; kp < RK / 32; ++kp) {
           uint32_t b0, b1, b2, b3;
-          gqa::ldsm_x4(sbase + gqa::swz<RK * 2>(row, 4 * kp + mid), b0, b1, b2, b3);
+          gqa::ldsm_x4(sb + gqa::swz<RK * 2>(row, 4 * kp + mid), b0, b1, b2, b3);
           gqa::mma16816(d, aq[2 * kp], b0, b1);
           gqa::mma16816(d, aq[2 * kp + 1], b2, b3);
         }
@@ -291,7 +299,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
         s[nb][0] = (t0 < tl.tn) ? d[0] + d[2] + bg : -CUDART_INF_F;
         s[nb][1] = (t0 + 1 < tl.tn) ? d[1] + d[3] + bg : -CUDART_INF_F;
       }
-      softmax_pv(NbV{}, s, sbase + C::KB, C::VH);
+      softmax_pv(NbV{}, s, sb + C::KB, C::VH);
     } else {
       float s[NbX::value][2];
 #pragma unroll
@@ -302,7 +310,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
         for (int kp = 0; kp < 4; ++kp) {
           const uint32_t ch = 4 * kp + mid;  // 16-byte chunk 0..15 of the 256-byte row
           uint32_t b0, b1, b2, b3;
-          gqa::ldsm_x4(sbase + (ch >> 3) * C::XH + gqa::swz<128>(row, ch & 7), b0, b1, b2, b3);
+          gqa::ldsm_x4(sb + (ch >> 3) * C::XH + gqa::swz<128>(row, ch & 7), b0, b1, b2, b3);
           gqa::mma16816(d, ax[2 * kp], b0, b1);
           gqa::mma16816(d, ax[2 * kp + 1], b2, b3);
         }
@@ -310,12 +318,12 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
         s[nb][0] = (t0 < tl.tn) ? d[0] + d[2] : -CUDART_INF_F;
         s[nb][1] = (t0 + 1 < tl.tn) ? d[1] + d[3] : -CUDART_INF_F;
       }
-      softmax_pv(NbX{}, s, sbase + 2 * C::XH, C::XH);
+      softmax_pv(NbX{}, s, sb + 2 * C::XH, C::XH);
     }
     __syncwarp();
     if (lane == 0 && px < b) {
       fence_proxy_async();
-      issue();
+      issue(st);
     }
     cx += tl.tn;
     ++j;
