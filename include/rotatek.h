@@ -69,10 +69,11 @@ enum {
                                      mu = 0, C = K^T K (north_star's literal wording)  */
   ROTATEK_QUERY_WEIGHT = 1u << 1, /* C_q = (sigma sigma^T) (.) C.  Off (or
                                      W == 0): sigma == 1, the K-only PCA arm   */
-  ROTATEK_EIG_FP32 = 1u << 2,     /* bf16 caches only: run the Jacobi eigensolver in fp32
-                                     (faster; projector error ~1e-4, which can exceed
-                                     the 2e-3 end-to-end gate on some data).  Default:
-                                     fp64 Jacobi (projector error ~1e-7)               */
+  ROTATEK_EIG_FP64 = 1u << 2,     /* run the whole Jacobi eigensolver in fp64 (always on for
+                                     fp32 caches).  Default for bf16 caches: fp32 parallel
+                                     Jacobi followed by one fp64 refinement step
+                                     (B = V0^T C_q V0, lambda = diag B, V = V0 (I + W) with
+                                     the first-order correction W_ij = B_ij / (B_jj - B_ii)) */
   ROTATEK_SIMT_ONLY = 1u << 8,    /* use the CUDA-core (SIMT) kernels instead of the tcgen05
                                      tensor-core ones (A/B tests and benches)           */
   ROTATEK_DEFAULT_FLAGS = (1u << 0) | (1u << 1)

@@ -87,7 +87,7 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const v
   const bool bf16 = dm->dtype == ROTATEK_BF16;
   const bool weight = (flags & ROTATEK_QUERY_WEIGHT) && W > 0;
   const bool center = (flags & ROTATEK_CENTER) != 0;
-  const bool fp64 = !bf16 || !(flags & ROTATEK_EIG_FP32);
+  const bool fp64 = !bf16 || (flags & ROTATEK_EIG_FP64);
   if (!K || !R || !dmu) return fail(ROTATEK_ERR_NULL, "K, R and dmu are required");
   if (W > 0 && !Qw) return fail(ROTATEK_ERR_DIMS, "Qw is NULL but q_window > 0");
   if (d > 128) return fail(ROTATEK_ERR_UNSUPPORTED, "calibrate supports head_dim <= 128");
@@ -105,7 +105,7 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const v
     return s;
   if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
   if ((s = launched(rk::launch_jacobi(U, d, fp64, ws, st), &n))) return s;
-  if ((s = launched(rk::launch_select_gather(U, d, r, fp64, bf16, center, ws, R, dmu, eigvals,
+  if ((s = launched(rk::launch_select_gather(U, d, r, /*fp64_vecs=*/true, bf16, center, ws, R, dmu, eigvals,
                                              keep_mask, keep_idx, R_full, info, st), &n)))
     return s;
   g_launches = n;

@@ -372,18 +372,288 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(int d, const dou
   if (tid == 0) jinfo[u] = converged ? 0 : (sweep > 0 ? sweep : 1);
 }
 
+// ------------------------------------------------------------------------------------------
+// fp32 Jacobi, full storage (row stride d+1: row and column passes are both bank-conflict
+// free), 1024 threads per CTA (one CTA per SM; 32 warps hide the shared-memory latency of the
+// rotation passes).  A round: (1) d/2 threads compute the Schur rotations of the round's
+// disjoint pairs, (2) row pass A <- J^T A over all (pair, column), (3) column pass A <- A J
+// and V <- V J over all (row, pair).  Followed by refine_kernel (fp64).
+constexpr int kJ32Threads = 1024;
+
+size_t jacobi32_smem_bytes(int d) {
+  const int h = d / 2;
+  return ((size_t)2 * d * (d + 1) + 3 * h + 32) * 4 + (size_t)2 * h * 2 + 64;
+}
+
+template <int DC>  // DC > 0: compile-time head dim (index math by shifts); 0: runtime d
+__global__ void __launch_bounds__(kJ32Threads, 1) jacobi32_kernel(int d_rt, const double* __restrict__ cq,
+                                                                  float* __restrict__ lam_out,
+                                                                  float* __restrict__ vecs,
+                                                                  int32_t* __restrict__ jinfo, float tol,
+                                                                  int max_sweeps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int d = DC > 0 ? DC : d_rt;
+  const int u = blockIdx.x, tid = threadIdx.x, nth = blockDim.x;
+  const int h = d / 2, ld = d + 1;
+  float* A = reinterpret_cast<float*>(smem_raw);
+  float* V = A + d * ld;
+  float* cs = V + d * ld;
+  float* sn = cs + h;
+  float* tt = sn + h;
+  float* red = tt + h;
+  uint16_t* Pp = reinterpret_cast<uint16_t*>(red + 32);
+  uint16_t* Qp = Pp + h;
+  __shared__ double s_red[32];
+  __shared__ int s_bad;
+
+  const double* C = cq + (size_t)u * d * d;
+  double f2 = 0.0;
+  int bad = 0;
+  for (int e = tid; e < d * d; e += nth) {
+    const double x = C[e];
+    if (!isfinite(x)) bad = 1;
+    f2 = fma(x, x, f2);
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  if (bad) s_bad = 1;
+  f2 = block_sum<double>(f2, s_red);
+  __syncthreads();
+  if (s_bad) {
+    for (int e = tid; e < d * d; e += nth) vecs[(size_t)u * d * d + e] = 0.f;
+    for (int j = tid; j < d; j += nth) lam_out[(size_t)u * d + j] = CUDART_NAN_F;
+    if (tid == 0) jinfo[u] = -1;
+    return;
+  }
+  int ex = 0;
+  if (f2 > 0.0) frexp(sqrt(f2), &ex);
+  const double scale = ldexp(1.0, -ex), unscale = ldexp(1.0, ex);
+  for (int e = tid; e < d * d; e += nth) {
+    const int i = e / d, j = e % d;
+    A[i * ld + j] = (float)(C[e] * scale);
+    V[i * ld + j] = (i == j) ? 1.f : 0.f;
+  }
+  __syncthreads();
+  float fro2 = 0.f;
+  for (int e = tid; e < d * d; e += nth) {
+    const float a = A[(e / d) * ld + (e % d)];
+    fro2 = fmaf(a, a, fro2);
+  }
+  fro2 = block_sum<float>(fro2, red);
+
+  int sweep = 0, converged = 0;
+  for (;; ++sweep) {
+    float off2 = 0.f;
+    for (int e = tid; e < d * d; e += nth) {
+      const int i = e / d, j = e % d;
+      if (i != j) {
+        const float a = A[i * ld + j];
+        off2 = fmaf(a, a, off2);
+      }
+    }
+    off2 = block_sum<float>(off2, red);
+    if (off2 <= tol * tol * fro2) { converged = 1; break; }
+    if (sweep >= max_sweeps) break;
+    for (int k = 0; k < d - 1; ++k) {
+      if (tid < h) {
+        int p, q;
+        if (tid == 0) { p = k; q = d - 1; }
+        else { p = (k + tid) % (d - 1); q = (k - tid + (d - 1)) % (d - 1); }
+        if (p > q) { const int t = p; p = q; q = t; }
+        const float apq = A[p * ld + q];
+        float c = 1.f, s = 0.f;
+        if (apq != 0.f) {
+          const float app = A[p * ld + p], aqq = A[q * ld + q];
+          const float tau = (aqq - app) / (2.f * apq);
+          const float t = (tau >= 0.f ? 1.f : -1.f) / (fabsf(tau) + sqrtf(1.f + tau * tau));
+          // correctly rounded sqrt + divide: rsqrtf's one-sided ulp error would drift the
+          // column norms of V by ~2e-4 over the ~1000 rotations a column receives
+          c = 1.f / sqrtf(1.f + t * t);
+          s = t * c;
+        }
+        cs[tid] = c; sn[tid] = s;
+        Pp[tid] = (uint16_t)p; Qp[tid] = (uint16_t)q;
+      }
+      __syncthreads();
+      // rows: A <- J^T A
+      for (int e = tid; e < h * d; e += nth) {
+        const int a = e / d, j = e % d;
+        const int p = Pp[a], q = Qp[a];
+        const float c = cs[a], s = sn[a];
+        const float x = A[p * ld + j], y = A[q * ld + j];
+        A[p * ld + j] = c * x - s * y;
+        A[q * ld + j] = s * x + c * y;
+      }
+      __syncthreads();
+      // columns: A <- A J, V <- V J
+      for (int e = tid; e < h * d; e += nth) {
+        const int b = e / d, i = e % d;
+        const int p = Pp[b], q = Qp[b];
+        const float c = cs[b], s = sn[b];
+        const float x = A[i * ld + p], y = A[i * ld + q];
+        A[i * ld + p] = c * x - s * y;
+        A[i * ld + q] = s * x + c * y;
+        const float vx = V[i * ld + p], vy = V[i * ld + q];
+        V[i * ld + p] = c * vx - s * vy;
+        V[i * ld + q] = s * vx + c * vy;
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = tid; j < d; j += nth) lam_out[(size_t)u * d + j] = (float)((double)A[j * ld + j] * unscale);
+  for (int e = tid; e < d * d; e += nth) vecs[(size_t)u * d * d + e] = V[(e / d) * ld + (e % d)];
+  if (tid == 0) jinfo[u] = converged ? 0 : (sweep > 0 ? sweep : 1);
+}
+
+// ------------------------------------------------------------------------------------------
+// fp64 refinement of the fp32 eigenbasis V0 (one Rayleigh-Ritz + first-order step):
+//   B = V0^T C V0 (fp64; C the fp64 C_q), lambda_i = B_ii,
+//   W_ij = B_ij / (B_jj - B_ii) (i != j; 0 where the pair is too close to separate),
+//   V = V0 (I + W).
+// B is diagonal up to the fp32 solver's residual eps ~ 1e-6 ||C||, so the step leaves an
+// O(eps^2 / gap^2) error: fp64-quality projectors at the cost of three 128^3 fp64 GEMMs.
+constexpr int kRefThreads = 256;
+
+__global__ void __launch_bounds__(kRefThreads) refine_kernel(int d, const double* __restrict__ cq,
+                                                              const float* __restrict__ v0g,
+                                                              double* __restrict__ scratch,
+                                                              float* __restrict__ lam_out,
+                                                              double* __restrict__ vout,
+                                                              const int32_t* __restrict__ jinfo) {
+  extern __shared__ __align__(16) float v0[];  // [d][d] fp32 (exact copy of the fp32 basis)
+  __shared__ double diag[256];
+  const int u = blockIdx.x, tid = threadIdx.x;
+  if (jinfo[u] == -1) return;  // non-finite input: nothing to refine (select zero-fills)
+  const double* C = cq + (size_t)u * d * d;
+  double* T = scratch + (size_t)u * d * d;   // C V0, then W
+  const float* V0 = v0g + (size_t)u * d * d;
+  for (int e = tid; e < d * d; e += blockDim.x) v0[e] = V0[e];
+  __syncthreads();
+  // 4x4 output tiles per thread over the d x d result
+  const int nt = d / 4;
+  // (1) T = C V0
+  for (int t = tid; t < nt * nt; t += blockDim.x) {
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+    double acc[4][4] = {};
+    for (int l = 0; l < d; ++l) {
+      double cv[4], vv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) cv[a] = C[(size_t)(i0 + a) * d + l];
+      const float4 v4 = *reinterpret_cast<const float4*>(v0 + l * d + j0);
+      vv[0] = v4.x; vv[1] = v4.y; vv[2] = v4.z; vv[3] = v4.w;
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(cv[a], vv[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) T[(size_t)(i0 + a) * d + j0 + b] = acc[a][b];
+  }
+  __syncthreads();
+  // (2) B = V0^T T into vout (scratch until step 4) and the Gram matrix G = V0^T V0 into
+  // the C_q buffer (C is no longer needed): the fp32 basis is orthonormal only to
+  // ~1e-6 per entry, so the step below solves B x = lambda G x to first order.
+  double* Bg = vout + (size_t)u * d * d;
+  double* Gg = const_cast<double*>(C);
+  for (int t = tid; t < nt * nt; t += blockDim.x) {
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+    double acc[4][4] = {}, gac[4][4] = {};
+    for (int k = 0; k < d; ++k) {
+      double vv[4], tv[4], ww[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) vv[a] = (double)v0[k * d + i0 + a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        tv[b] = T[(size_t)k * d + j0 + b];
+        ww[b] = (double)v0[k * d + j0 + b];
+      }
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          acc[a][b] = fma(vv[a], tv[b], acc[a][b]);
+          gac[a][b] = fma(vv[a], ww[b], gac[a][b]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        Bg[(size_t)(i0 + a) * d + j0 + b] = acc[a][b];
+        Gg[(size_t)(i0 + a) * d + j0 + b] = gac[a][b];
+        if (i0 + a == j0 + b) diag[i0 + a] = acc[a][b] / gac[a][b];  // Rayleigh quotient
+      }
+  }
+  __syncthreads();
+  // (3) first-order correction of B x = lambda G x into T (C V0 is no longer needed):
+  //   W_ij = (B_ij - lambda_j G_ij) / (lambda_j - lambda_i)  (i != j),  W_jj = (1 - G_jj) / 2
+  double bmax = 0.0;
+  for (int i = 0; i < d; ++i) bmax = fmax(bmax, fabs(diag[i]));
+  for (int e = tid; e < d * d; e += blockDim.x) {
+    const int i = e / d, j = e % d;
+    const double num = Bg[e] - diag[j] * Gg[e];
+    const double gap = diag[j] - diag[i];
+    double w;
+    if (i == j) w = 0.5 * (1.0 - Gg[e]);
+    else if (fabs(gap) > 1e-12 * bmax && fabs(num) < 0.1 * fabs(gap)) w = num / gap;
+    else w = 0.0;
+    T[e] = w;
+  }
+  __syncthreads();
+  // (4) V = V0 + V0 W
+  for (int t = tid; t < nt * nt; t += blockDim.x) {
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = (double)v0[(i0 + a) * d + j0 + b];
+    for (int k = 0; k < d; ++k) {
+      double vv[4], wv[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) vv[a] = (double)v0[(i0 + a) * d + k];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) wv[b] = T[(size_t)k * d + j0 + b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = fma(vv[a], wv[b], acc[a][b]);
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) Bg[(size_t)(i0 + a) * d + j0 + b] = acc[a][b];
+  }
+  for (int j = tid; j < d; j += blockDim.x) lam_out[(size_t)u * d + j] = (float)diag[j];
+}
+
 int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st) {
-  size_t sm = jacobi_smem_bytes(d, fp64);
   if (fp64) {
+    size_t sm = jacobi_smem_bytes(d, true);
     cudaFuncSetAttribute(jacobi_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     jacobi_kernel<double><<<U, kJacobiThreads, sm, st>>>(d, ws.cq, ws.lam, (double*)ws.vecs,
                                                          ws.jinfo, 1e-13, 40);
-  } else {
-    cudaFuncSetAttribute(jacobi_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    jacobi_kernel<float><<<U, kJacobiThreads, sm, st>>>(d, ws.cq, ws.lam, (float*)ws.vecs,
-                                                        ws.jinfo, 1e-6f, 30);
+    return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
   }
-  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+  // fp32 solve into ws.v32, then the fp64 refinement writes the fp64 basis into ws.vecs;
+  // covpart (>= U d^2 doubles) is the refinement's per-unit scratch.
+  float* v32 = ws.v32;
+  size_t sm = jacobi32_smem_bytes(d);
+  if (d == 128) {
+    cudaFuncSetAttribute(jacobi32_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    jacobi32_kernel<128><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
+  } else {
+    cudaFuncSetAttribute(jacobi32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    jacobi32_kernel<0><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return -1;
+  const size_t rsm = (size_t)d * d * 4;
+  cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+  refine_kernel<<<U, kRefThreads, rsm, st>>>(d, ws.cq, v32, ws.covpart, ws.lam,
+                                             static_cast<double*>(ws.vecs), ws.jinfo);
+  return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
 }
 
 // ============================================================== step 5: top-r select
@@ -560,6 +830,7 @@ size_t calib_ws_layout(int U, int d, int N, bool fp64_eig, void* base, CalibWs* 
   w.mu = (double*)take((size_t)U * d * 8);
   w.lam = (float*)take((size_t)U * d * 4);
   w.vecs = take((size_t)U * d * d * (fp64_eig ? 8 : 4));
+  w.v32 = (float*)take((size_t)U * d * d * 4);
   w.jinfo = (int32_t*)take((size_t)U * 4);
   if (ws) *ws = w;
   return off;

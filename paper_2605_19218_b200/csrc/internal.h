@@ -16,7 +16,8 @@ struct CalibWs {
   double* cq;        // [U, d, d]
   double* mu;        // [U, d]
   float* lam;        // [U, d]
-  void* vecs;        // [U, d, d] float or double
+  void* vecs;        // [U, d, d] double (eigenvectors, columns in solver order)
+  float* v32;        // [U, d, d] fp32 Jacobi basis before the fp64 refinement
   int32_t* jinfo;    // [U]
   int parts;         // P token partitions per unit
 };

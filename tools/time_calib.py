@@ -1,0 +1,19 @@
+"""Time rotatek_calibrate phases for a config with different flags (experiments)."""
+import os, sys, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import paper_2605_19218_b200 as rk
+from workload import CONFIGS, make_workload
+
+cfg = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "llava_b32"]
+w = make_workload(cfg, threads=os.cpu_count() or 8)
+def dev(t):
+    return torch.from_numpy(np.ascontiguousarray(t.bits).view(np.int16)).view(torch.bfloat16).cuda()
+K, Qw = dev(w["K"]), dev(w["Qw"])
+for name, flags in [("fp32-jacobi+fp64-refine", rk.DEFAULT_FLAGS), ("fp64-jacobi", rk.DEFAULT_FLAGS | rk.EIG_FP64)]:
+    for it in range(3):
+        torch.cuda.synchronize(); t0 = time.perf_counter()
+        cal = rk.calibrate(K, Qw, cfg.rank, flags)
+        torch.cuda.synchronize(); t1 = time.perf_counter()
+    info = cal["info"].cpu().numpy()
+    print(f"{cfg.name} {name}: {1e3*(t1-t0):.2f} ms  info>0: {(info>0).sum()}  info<0: {(info<0).sum()}")
