@@ -420,6 +420,65 @@ void orc_decode(int U, int G, int d, int r, int N, int M, const double* q, const
     }
 }
 
+/* ------------------------------------------------------------------------ */
+/* NEXT-1: the paper's default solver, Cholesky-QR subspace iteration        */
+/* (Alg. 1 lines 6-13; Sec. 3.3; App. E):               */
+/*   V <- V0 (given: "Sample V with i.i.d. N(0,1) entries" -- the random     */
+/*        numbers are an input so both sides use the same draw)               */
+/*   repeat T times:  V <- C_q V ; G <- V^T V ; rho <- eps tr(G) / k ;         */
+/*                    L <- Cholesky(G + rho I) ; V <- V L^{-T}                 */
+/*   R_k <- V                                                                 */
+/* One unit: C [d][d], V0 [d][k], out Rk [d][k].  Returns 0, or -1 if a       */
+/* Cholesky pivot is not positive.                                           */
+/* ------------------------------------------------------------------------ */
+int orc_subspace(const double* C, const double* V0, int d, int k, int T, double eps, double* Rk) {
+  double* V = (double*)malloc(sizeof(double) * (size_t)d * k);
+  double* W = (double*)malloc(sizeof(double) * (size_t)d * k);
+  double* G = (double*)malloc(sizeof(double) * (size_t)k * k);
+  double* L = (double*)calloc((size_t)k * k, sizeof(double));
+  int rc = 0;
+  memcpy(V, V0, sizeof(double) * (size_t)d * k);
+  for (int t = 0; t < T && rc == 0; ++t) {
+    for (int i = 0; i < d; ++i) /* V <- C V */
+      for (int j = 0; j < k; ++j) {
+        double s = 0.0;
+        for (int l = 0; l < d; ++l) s += C[IDX2(i, l, d)] * V[IDX2(l, j, k)];
+        W[IDX2(i, j, k)] = s;
+      }
+    for (int a = 0; a < k; ++a) /* G <- V^T V */
+      for (int b = 0; b < k; ++b) {
+        double s = 0.0;
+        for (int i = 0; i < d; ++i) s += W[IDX2(i, a, k)] * W[IDX2(i, b, k)];
+        G[IDX2(a, b, k)] = s;
+      }
+    double tr = 0.0; /* rho <- eps tr(G) / k */
+    for (int a = 0; a < k; ++a) tr += G[IDX2(a, a, k)];
+    const double rho = eps * tr / (double)k;
+    for (int a = 0; a < k; ++a) G[IDX2(a, a, k)] += rho;
+    for (int j = 0; j < k && rc == 0; ++j) { /* L <- Cholesky(G + rho I), G = L L^T */
+      double s = G[IDX2(j, j, k)];
+      for (int m = 0; m < j; ++m) s -= L[IDX2(j, m, k)] * L[IDX2(j, m, k)];
+      if (!(s > 0.0)) { rc = -1; break; }
+      L[IDX2(j, j, k)] = sqrt(s);
+      for (int i = j + 1; i < k; ++i) {
+        double v = G[IDX2(i, j, k)];
+        for (int m = 0; m < j; ++m) v -= L[IDX2(i, m, k)] * L[IDX2(j, m, k)];
+        L[IDX2(i, j, k)] = v / L[IDX2(j, j, k)];
+      }
+    }
+    if (rc) break;
+    for (int i = 0; i < d; ++i) /* V <- W L^{-T}: each row x solves x L^T = w */
+      for (int j = 0; j < k; ++j) {
+        double s = W[IDX2(i, j, k)];
+        for (int m = 0; m < j; ++m) s -= V[IDX2(i, m, k)] * L[IDX2(j, m, k)];
+        V[IDX2(i, j, k)] = s / L[IDX2(j, j, k)];
+      }
+  }
+  memcpy(Rk, V, sizeof(double) * (size_t)d * k);
+  free(V); free(W); free(G); free(L);
+  return rc;
+}
+
 /* KV-budget multiplier of tab:main_comparison: keys pruned to  */
 /* channel_keep of their channels, values kept full, so the visual cache    */
 /* shrinks by token_keep * (1 + channel_keep) / 2.                           */

@@ -69,6 +69,8 @@ def lib():
             L.orc_decode.argtypes = [i, i, i, i, i, i, dp, dp, dp, dp, dp, dp, dp,
                                      ctypes.c_double, dp]
             L.orc_scores.argtypes = [i, i, i, i, i, i, dp, dp, dp, dp, dp, ctypes.c_double, dp]
+            L.orc_subspace.argtypes = [dp, dp, i, i, i, ctypes.c_double, dp]
+            L.orc_subspace.restype = ctypes.c_int
             L.orc_budget.argtypes = [ctypes.c_double, ctypes.c_double]
             L.orc_budget.restype = ctypes.c_double
             _lib = L
@@ -253,6 +255,46 @@ def scores(q, Kt, R, dmu, Ktext=None, scale=0.0) -> np.ndarray:
     lib().orc_scores(U, G, d, r, N, M, _p(q), _p(Kt), _p(R), None if dm is None else _p(dm),
                      _p(Ktext), float(scale), _p(out))
     return out
+
+
+SUBSPACE_T = 5          # "T = 5 iterations"
+SUBSPACE_EPS = 1e-6     # ridge factor: unspecified in the paper; SPEC's default
+
+
+def subspace(Cq, V0, T=SUBSPACE_T, eps=SUBSPACE_EPS):
+    """NEXT-1, Alg. 1 lines 6-13: Cholesky-QR subspace iteration from the given V0.
+    Cq [U, d, d] (or [d, d]), V0 [U, d, k] (or [d, k]) -> R_k of the same shape as V0.
+    Returns None if a Cholesky pivot fails."""
+    Cq = _f64(Cq)
+    V0 = _f64(V0)
+    single = Cq.ndim == 2
+    if single:
+        Cq, V0 = Cq[None], V0[None]
+    U, d, k = V0.shape
+    out = np.empty((U, d, k))
+    for u in range(U):
+        c = np.ascontiguousarray(Cq[u])
+        v = np.ascontiguousarray(V0[u])
+        o = np.empty((d, k))
+        if lib().orc_subspace(_p(c), _p(v), d, k, int(T), float(eps), _p(o)) != 0:
+            return None
+        out[u] = o
+    return out[0] if single else out
+
+
+def calibrate_subspace(K, Qw, V0, T=SUBSPACE_T, eps=SUBSPACE_EPS, center=True,
+                       query_weight=True) -> dict:
+    """Alg. 1 with the paper's default solver: steps 1-5 as in calibrate(), the basis from
+    subspace(), then delta_mu = mu - R R^T mu (line 15)."""
+    K = _f64(K)
+    U, N, d = K.shape
+    if Qw is None or not query_weight:
+        Qw = np.zeros((U, 1, 0, d))
+    sig = query_sigma(Qw)
+    mu, C = mean_cov(K, center)
+    Cq = hadamard(C, sig)
+    R = subspace(Cq, V0, T, eps)
+    return dict(sigma=sig, mu=mu, Cq=Cq, R=R, dmu=dmu_from_R(R, mu) if center else np.zeros((U, d)))
 
 
 def budget(token_keep: float, channel_keep: float) -> float:
