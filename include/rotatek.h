@@ -130,6 +130,27 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dims, uint32_t flags, const
                                  rotatek_stream_t stream);
 
 /*
+ * The paper's default solver (NEXT-1): Alg. 1 lines 1-5 as in rotatek_calibrate, then the
+ * Cholesky-QR subspace iteration of lines 6-13:
+ *   V <- V0; T times { V <- C_q V; G <- V^T V; rho <- eps tr(G)/r; L <- chol(G + rho I);
+ *                      V <- V L^{-T} };  R_r <- V;  dmu = mu - R_r R_r^T mu (from stored R_r)
+ *   V0     [U, d, r] fp32 device: the start basis ("Sample V with i.i.d. N(0,1) entries",
+ *          l.6) -- the random draw is an input, so results are reproducible
+ *   iters  T (<= 0: 5);  ridge eps (< 0: 1e-6; unspecified in the paper)
+ *   R      [U, d, r] fp32 out;  dmu [U, d] fp32 out
+ *   ritz   [U, r] fp32 out (nullable): Rayleigh quotients R_j^T C_q R_j / R_j^T R_j
+ *   info   [U] (nullable): 0, or -1 if a Cholesky pivot was not positive
+ * There is no eigen-index selection here, so no head mask / kept indices are produced.
+ * Errors: NULL, DIMS, ALIGN, WORKSPACE (rotatek_workspace_bytes(.., OP_CALIBRATE)),
+ * UNSUPPORTED (d > 128 or r not in {4, 8, 16, 32, 64}), CUDA.
+ */
+rotatek_status rotatek_calibrate_subspace(const rotatek_dims* dims, uint32_t flags, const void* K,
+                                          const void* Qw, const float* V0, int32_t iters,
+                                          float ridge, float* R, float* dmu, float* ritz,
+                                          int32_t* info, void* workspace, size_t workspace_bytes,
+                                          rotatek_stream_t stream);
+
+/*
  * Alg. 1 line 14: K~ = RNE_dtype(K R_r), over the UNCENTERED K.
  *   K      [U, N, d]  dims->dtype
  *   R      [U, d, r]  fp32 as written by rotatek_calibrate

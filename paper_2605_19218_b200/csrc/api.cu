@@ -112,6 +112,44 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const v
   return ROTATEK_OK;
 }
 
+rotatek_status rotatek_calibrate_subspace(const rotatek_dims* dm, uint32_t flags, const void* K,
+                                          const void* Qw, const float* V0, int32_t iters,
+                                          float ridge, float* R, float* dmu, float* ritz,
+                                          int32_t* info, void* workspace, size_t workspace_bytes,
+                                          rotatek_stream_t stream) {
+  g_launches = 0;
+  rotatek_status s = check_dims(dm);
+  if (s != ROTATEK_OK) return s;
+  const int U = dm->units, G = dm->group, d = dm->head_dim, r = dm->rank, N = dm->n_vis,
+            W = dm->q_window;
+  const bool bf16 = dm->dtype == ROTATEK_BF16;
+  const bool weight = (flags & ROTATEK_QUERY_WEIGHT) && W > 0;
+  const bool center = (flags & ROTATEK_CENTER) != 0;
+  if (!K || !V0 || !R || !dmu) return fail(ROTATEK_ERR_NULL, "K, V0, R and dmu are required");
+  if (W > 0 && !Qw) return fail(ROTATEK_ERR_DIMS, "Qw is NULL but q_window > 0");
+  if (d > 128 || !(r == 4 || r == 8 || r == 16 || r == 32 || r == 64))
+    return fail(ROTATEK_ERR_UNSUPPORTED, "subspace solver: head_dim <= 128, rank in {4,8,16,32,64}");
+  const void* ptrs[] = {K, Qw, V0, R, dmu, ritz, info, workspace};
+  for (const void* p : ptrs)
+    if (p && !aligned16(p)) return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
+  rk::CalibWs ws;
+  const size_t need = rk::calib_ws_layout(U, d, N, true, workspace, &ws);
+  if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const int T = iters > 0 ? iters : 5;
+  const double eps = ridge >= 0.f ? (double)ridge : 1e-6;
+  int n = 0;
+  if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
+  const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::cov_tc_supported(d, bf16);
+  if ((s = launched(tc ? rk::launch_cov_tc(U, N, K, ws, st) : rk::launch_cov(U, N, d, bf16, K, ws, st), &n)))
+    return s;
+  if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
+  if ((s = launched(rk::launch_subspace(U, d, r, T, eps, center, ws, V0, R, dmu, ritz, info, st), &n)))
+    return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
 rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dm, const void* K, const float* R,
                                       void* K_comp, uint32_t flags, rotatek_stream_t stream) {
   g_launches = 0;

@@ -49,6 +49,8 @@ int launch_select_gather(int U, int d, int r, bool fp64_vecs, bool bf16x2, bool 
                          const CalibWs& ws, float* R, float* dmu, float* eigvals,
                          uint32_t* mask, int32_t* idx, float* R_full, int32_t* info,
                          cudaStream_t st);
+int launch_subspace(int U, int d, int k, int iters, double eps, bool center, const CalibWs& ws,
+                    const float* V0, float* R, float* dmu, float* ritz, int32_t* info, cudaStream_t st);
 int launch_select_only(int U, int d, int r, const float* lam, uint32_t* mask, int32_t* idx,
                        int32_t* info, cudaStream_t st);
 int launch_compress(int U, int N, int d, int r, bool bf16, const void* K, const float* R,

@@ -60,6 +60,9 @@ def lib():
             L.rotatek_workspace_bytes.argtypes = [dp, ctypes.c_int]
             L.rotatek_workspace_bytes.restype = sz
             L.rotatek_calibrate.argtypes = [dp, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp]
+            L.rotatek_calibrate_subspace.argtypes = [dp, u32, vp, vp, vp, i32, f, vp, vp, vp, vp,
+                                                     vp, sz, vp]
+            L.rotatek_calibrate_subspace.restype = ctypes.c_int
             L.rotatek_compress_kv.argtypes = [dp, vp, vp, vp, vp]
             L.rotatek_compress_kv_ex.argtypes = [dp, vp, vp, vp, u32, vp]
             L.rotatek_decode_attn.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz, vp]
@@ -170,6 +173,33 @@ def calibrate(K: torch.Tensor, Qw: torch.Tensor | None, rank: int, flags: int = 
                                    _ptr(out["eigvals"]), _ptr(out["mask"]), _ptr(out["idx"]),
                                    _ptr(out["R_full"]), _ptr(out["info"]), _ptr(ws), ws.numel(),
                                    _stream(stream)))
+    return out
+
+
+def calibrate_subspace(K: torch.Tensor, Qw: torch.Tensor | None, V0: torch.Tensor,
+                       flags: int = DEFAULT_FLAGS, iters: int = 5, ridge: float = 1e-6, *,
+                       ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Alg. 1 with the paper's default solver (Cholesky-QR subspace iteration from V0).
+    K [U, N, d]; Qw [U, G, W, d] or None; V0 [U, d, r] f32 -> dict(R, dmu, ritz, info)."""
+    U, N, d = K.shape
+    r = V0.shape[2]
+    assert V0.shape == (U, d, r) and V0.dtype == torch.float32
+    if Qw is None:
+        G, W = 1, 0
+    else:
+        G, W = Qw.shape[1], Qw.shape[2]
+    dims = make_dims(U, G, d, r, N, 0, W, _dtype_code(K))
+    dev = K.device
+    out = dict(R=torch.empty((U, d, r), dtype=torch.float32, device=dev),
+               dmu=torch.empty((U, d), dtype=torch.float32, device=dev),
+               ritz=torch.empty((U, r), dtype=torch.float32, device=dev),
+               info=torch.empty((U,), dtype=torch.int32, device=dev))
+    if ws is None:
+        ws = workspace(dims, OP_CALIBRATE, dev)
+    _check(lib().rotatek_calibrate_subspace(
+        ctypes.byref(dims), flags, _ptr(K), _ptr(Qw) if W > 0 else None, _ptr(V0), int(iters),
+        float(ridge), _ptr(out["R"]), _ptr(out["dmu"]), _ptr(out["ritz"]), _ptr(out["info"]),
+        _ptr(ws), ws.numel(), _stream(stream)))
     return out
 
 

@@ -17,3 +17,11 @@ for name, flags in [("fp32-jacobi+fp64-refine", rk.DEFAULT_FLAGS), ("fp64-jacobi
         torch.cuda.synchronize(); t1 = time.perf_counter()
     info = cal["info"].cpu().numpy()
     print(f"{cfg.name} {name}: {1e3*(t1-t0):.2f} ms  info>0: {(info>0).sum()}  info<0: {(info<0).sum()}")
+
+from workload.gen import draw_v0
+V0 = torch.from_numpy(draw_v0(cfg)).cuda()
+for it in range(3):
+    torch.cuda.synchronize(); t0 = time.perf_counter()
+    cal = rk.calibrate_subspace(K, Qw, V0)
+    torch.cuda.synchronize(); t1 = time.perf_counter()
+print(f"{cfg.name} subspace(T=5): {1e3*(t1-t0):.2f} ms  info<0: {(cal['info'].cpu().numpy()<0).sum()}")

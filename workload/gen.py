@@ -215,6 +215,19 @@ def make_workload(cfg: Config, seed: int | None = None, layer: int = 0, units=No
     return out
 
 
+def draw_v0(cfg: Config, seed: int | None = None, units=None) -> np.ndarray:
+    """Start basis of the subspace iteration ("Sample V with i.i.d. N(0,1) entries", Alg. 1
+    l.6): float32 [U, d, r], one generator per unit (stream 1 of default_rng([seed, u, 1]))."""
+    if seed is None:
+        seed = 1000 * cfg.config_id
+    ulist = list(range(cfg.units)) if units is None else [int(x) for x in units]
+    out = np.empty((len(ulist), cfg.head_dim, cfg.rank), np.float32)
+    for i, u in enumerate(ulist):
+        out[i] = np.random.default_rng([int(seed), int(u), 1]).standard_normal(
+            (cfg.head_dim, cfg.rank), dtype=np.float32)
+    return out
+
+
 def decode_bytes(cfg: Config) -> int:
     """Algorithmic bytes one decode launch must move:
     K~ U*N*r*s + V U*N*d*s + text 2*U*M*d*s + R_r U*d*r*4 + dmu U*d*4
