@@ -317,41 +317,52 @@ def run_ours(args):
     # ---------------- timed region B: the full hot path per layer (rows 1-8), phase events
     full = None
     if not args.skip_full:
+        from workload.gen import draw_v0
         calws = torch.zeros(rk.workspace_bytes(
             rk.make_dims(cfg.units, cfg.group, cfg.head_dim, cfg.rank, cfg.n_vis, 0,
                          cfg.q_window, dims.dtype), rk.OP_CALIBRATE), dtype=torch.uint8,
             device=dev)
+        V0 = torch.from_numpy(draw_v0(cfg, units=rank_units(cfg, rank))).to(dev)
         n_full = max(2, min(5, args.steps))
-        phase_ms = {"calibrate": 0.0, "compress": 0.0, "decode": 0.0}
-        for it in range(1 + n_full):
-            evs = []
-            with torch.cuda.stream(stream):
-                for ly in layers:
-                    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-                    e[0].record(stream)
-                    cal = rk.calibrate(ly["K"], ly["Qw"], cfg.rank, ws=calws, stream=stream)
-                    e[1].record(stream)
-                    rk.compress_kv(ly["K"], cal["R"], out=ly["Kc"], stream=stream)
-                    e[2].record(stream)
-                    rk.decode_attn(ly["q"], ly["Kc"], ly["V"], cal["R"], cal["dmu"], ly["Ktext"],
-                                   ly["Vtext"], out=ly["out"], ws=ws, stream=stream)
-                    e[3].record(stream)
-                    evs.append(e)
-            torch.cuda.synchronize()
-            if it == 0:
-                continue  # warm-up pass
-            for e in evs:
-                phase_ms["calibrate"] += e[0].elapsed_time(e[1])
-                phase_ms["compress"] += e[1].elapsed_time(e[2])
-                phase_ms["decode"] += e[2].elapsed_time(e[3])
-        per_layer_us = {k: round(1e3 * v / (n_full * L), 2) for k, v in phase_ms.items()}
-        step_ms = sum(phase_ms.values()) / n_full
-        cb = compress_bytes(cfg)
-        full = {"ms_per_step": round(step_ms, 3), "layers": L,
-                "us_per_layer": per_layer_us,
-                "prefill_tokens_per_s": round(cfg.units * cfg.n_vis /
-                                              ((per_layer_us["calibrate"] + per_layer_us["compress"]) * 1e-6), 1),
-                "compress_gbs_1pass_bytes": round(cb / (per_layer_us["compress"] * 1e-6) / 1e9, 1)}
+
+        def full_path(calibrate):
+            phase_ms = {"calibrate": 0.0, "compress": 0.0, "decode": 0.0}
+            for it in range(1 + n_full):
+                evs = []
+                with torch.cuda.stream(stream):
+                    for ly in layers:
+                        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+                        e[0].record(stream)
+                        cal = calibrate(ly)
+                        e[1].record(stream)
+                        rk.compress_kv(ly["K"], cal["R"], out=ly["Kc"], stream=stream)
+                        e[2].record(stream)
+                        rk.decode_attn(ly["q"], ly["Kc"], ly["V"], cal["R"], cal["dmu"],
+                                       ly["Ktext"], ly["Vtext"], out=ly["out"], ws=ws, stream=stream)
+                        e[3].record(stream)
+                        evs.append(e)
+                torch.cuda.synchronize()
+                if it == 0:
+                    continue  # warm-up pass
+                for e in evs:
+                    phase_ms["calibrate"] += e[0].elapsed_time(e[1])
+                    phase_ms["compress"] += e[1].elapsed_time(e[2])
+                    phase_ms["decode"] += e[2].elapsed_time(e[3])
+            per_layer_us = {k: round(1e3 * v / (n_full * L), 2) for k, v in phase_ms.items()}
+            cb = compress_bytes(cfg)
+            return {"ms_per_step": round(sum(phase_ms.values()) / n_full, 3), "layers": L,
+                    "us_per_layer": per_layer_us,
+                    "prefill_tokens_per_s": round(cfg.units * cfg.n_vis / (
+                        (per_layer_us["calibrate"] + per_layer_us["compress"]) * 1e-6), 1),
+                    "compress_gbs_1pass_bytes": round(cb / (per_layer_us["compress"] * 1e-6) / 1e9, 1)}
+
+        full = {"solver": "parallel Jacobi (fp32) + fp64 refinement (north_star; eigh arm P:653)"}
+        full.update(full_path(lambda ly: rk.calibrate(ly["K"], ly["Qw"], cfg.rank, ws=calws,
+                                                      stream=stream)))
+        sub = {"solver": "Cholesky-QR subspace iteration, T=5 (paper default, NEXT-1)"}
+        sub.update(full_path(lambda ly: rk.calibrate_subspace(ly["K"], ly["Qw"], V0, ws=calws,
+                                                              stream=stream)))
+        full["subspace_solver"] = sub
 
     # ---------------- e2e: full path from pinned host buffers, H2D/D2H inside the timed region
     e2e = None
