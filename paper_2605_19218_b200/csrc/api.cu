@@ -101,9 +101,11 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const v
   int n = 0;
   if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
   const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::cov_tc_supported(d, bf16);
-  if ((s = launched(tc ? rk::launch_cov_tc(U, N, K, ws, st) : rk::launch_cov(U, N, d, bf16, K, ws, st), &n)))
+  if ((s = launched(tc ? rk::launch_cov_tc(U, N, center, K, ws, st) : rk::launch_cov(U, N, d, bf16, K, ws, st),
+                    &n)))
     return s;
-  if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
+  if (!(tc && ws.parts == 1))  // the tensor-core kernel finalizes in place when one CTA sees the unit
+    if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
   if ((s = launched(rk::launch_jacobi(U, d, fp64, ws, st), &n))) return s;
   if ((s = launched(rk::launch_select_gather(U, d, r, /*fp64_vecs=*/true, bf16, center, ws, R, dmu, eigvals,
                                              keep_mask, keep_idx, R_full, info, st), &n)))
@@ -141,9 +143,11 @@ rotatek_status rotatek_calibrate_subspace(const rotatek_dims* dm, uint32_t flags
   int n = 0;
   if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
   const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::cov_tc_supported(d, bf16);
-  if ((s = launched(tc ? rk::launch_cov_tc(U, N, K, ws, st) : rk::launch_cov(U, N, d, bf16, K, ws, st), &n)))
+  if ((s = launched(tc ? rk::launch_cov_tc(U, N, center, K, ws, st) : rk::launch_cov(U, N, d, bf16, K, ws, st),
+                    &n)))
     return s;
-  if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
+  if (!(tc && ws.parts == 1))  // the tensor-core kernel finalizes in place when one CTA sees the unit
+    if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
   if ((s = launched(rk::launch_subspace(U, d, r, T, eps, center, ws, V0, R, dmu, ritz, info, st), &n)))
     return s;
   g_launches = n;

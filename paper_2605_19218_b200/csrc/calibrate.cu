@@ -164,11 +164,14 @@ __global__ void __launch_bounds__(256) finalize_kernel(int N, int d, int parts, 
     for (int p = 0; p < parts; ++p) s += colpart[((size_t)u * parts + p) * d + j];
     double m = center ? s / (double)N : 0.0;
     sh_mu[j] = m;
-    mu_out[(size_t)u * d + j] = m;
+    if (blockIdx.y == 0) mu_out[(size_t)u * d + j] = m;
     sh_sig[j] = sigma[(size_t)u * d + j];
   }
   __syncthreads();
-  for (int e = threadIdx.x; e < d * d; e += blockDim.x) {
+  // blockIdx.y selects a band of rows (grid U x gridDim.y: enough CTAs even for small U)
+  const int rows = (d + gridDim.y - 1) / gridDim.y;
+  const int e0 = blockIdx.y * rows * d, e1 = min(d, (int)(blockIdx.y + 1) * rows) * d;
+  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
     int i = e / d, j = e % d;
     int a = min(i, j), b = max(i, j);
     double s = 0.0;
@@ -179,7 +182,7 @@ __global__ void __launch_bounds__(256) finalize_kernel(int N, int d, int parts, 
 }
 
 int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st) {
-  finalize_kernel<<<U, 256, 2 * d * sizeof(double), st>>>(N, d, ws.parts, center, ws.covpart,
+  finalize_kernel<<<dim3(U, 16), 256, 2 * d * sizeof(double), st>>>(N, d, ws.parts, center, ws.covpart,
                                                           ws.colpart, ws.sigma, ws.cq, ws.mu);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }

@@ -24,6 +24,7 @@ namespace {
 constexpr int kTK = 128;                 // tokens per chunk (fp32 accumulation window)
 constexpr int kDc = 128;                 // head dim
 constexpr int kStages = 4;
+constexpr int kWin = 2;                  // chunks per fp32 TMEM accumulation window (256 tokens)
 constexpr int kHalfBytes = kTK * 128;    // one 64-channel half: kTK rows x 128 B
 constexpr int kStageBytes = 2 * kHalfBytes;
 constexpr int kThreads = 320;
@@ -32,7 +33,10 @@ constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
 
 __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_constant__ CUtensorMap tmap, int N,
                                                              int parts, double* __restrict__ covpart,
-                                                             double* __restrict__ colpart) {
+                                                             double* __restrict__ colpart,
+                                                             const double* __restrict__ sigma,
+                                                             double* __restrict__ cq, double* __restrict__ mu,
+                                                             bool center, bool fused) {
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
@@ -40,7 +44,8 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ double colred[2][kDc];
+  __shared__ double colred[16][kDc];
+  __shared__ double colsum_sm[kDc];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.y, p = blockIdx.x;
@@ -84,19 +89,21 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 128, true, true);
       for (int i = 0; i < nch; ++i) {
-        const int s = i % kStages, a = i & 1;
+        // fp32 accumulation window = kWin chunks (kWin * 128 tokens <= 256, E-6)
+        const int s = i % kStages, wi = i / kWin, a = wi & 1;
+        const bool first = (i % kWin) == 0, last = (i % kWin) == kWin - 1 || i == nch - 1;
         mbar_wait(&full[s], (i / kStages) & 1);
-        mbar_wait(&tempty[a], ((i >> 1) & 1) ^ 1);
+        if (first) mbar_wait(&tempty[a], ((wi >> 1) & 1) ^ 1);
         tc::fence_after();
         const uint32_t base = smem_u32(sm + s * kStageBytes);
 #pragma unroll
         for (int kk = 0; kk < kTK / 16; ++kk) {
           // MN-major, SWIZZLE_128B: LBO = next 64-channel half, SBO = next 8-token group
           const uint64_t desc = tc::smem_desc(base + kk * 16 * 128, kHalfBytes, 1024, tc::SWZ_128B);
-          tc::mma_bf16(tmem + a * 128, desc, desc, idesc, kk > 0 ? 1u : 0u);
+          tc::mma_bf16(tmem + a * 128, desc, desc, idesc, (first && kk == 0) ? 0u : 1u);
         }
         tc::commit(&empty[s]);
-        tc::commit(&tfull[a]);
+        if (last) tc::commit(&tfull[a]);
       }
     }
   } else {
@@ -105,55 +112,90 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     const int q = warp & 3;        // TMEM lane quadrant this warp may access
     const int h = e >> 2;          // accumulator column half
     const int row = 32 * q + lane;  // output row (channel i)
-    const int cch = (e * 32 + lane) & (kDc - 1);  // colsum channel
-    const int thalf = (e * 32 + lane) >> 7;       // colsum token half (0..1)
+    const int et = e * 32 + lane;   // 0..255
+    const int c8 = et & 15;         // column sums: 8-channel chunk ...
+    const int rg = et >> 4;         // ... over token rows rg, rg + 16, ... of the chunk
     double acc[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) acc[j] = 0.0;
-    double csum = 0.0;
+    double csum[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) csum[j] = 0.0;
     for (int i = 0; i < nch; ++i) {
-      const int s = i % kStages, a = i & 1;
-      // column sums from the staged (swizzled) tile
+      const int s = i % kStages, wi = i / kWin, a = wi & 1;
+      const bool last = (i % kWin) == kWin - 1 || i == nch - 1;
+      // column sums from the staged (swizzled) tile: 16-byte loads, conflict-free
       mbar_wait(&full[s], (i / kStages) & 1);
       {
-        const unsigned char* half = sm + s * kStageBytes + (cch >> 6) * kHalfBytes;
-        const int c64 = cch & 63, chunk = c64 >> 3, within = (c64 & 7) * 2;
-        float fs = 0.f;
-#pragma unroll 8
-        for (int t = 0; t < 64; ++t) {
-          const int n = thalf * 64 + t;
-          const uint16_t v = *reinterpret_cast<const uint16_t*>(half + n * 128 + ((chunk ^ (n & 7)) << 4) + within);
-          fs += __uint_as_float((uint32_t)v << 16);
+        const unsigned char* half = sm + s * kStageBytes + (c8 >> 3) * kHalfBytes;
+        const int chunk = c8 & 7;
+        float fs[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) fs[j] = 0.f;
+#pragma unroll
+        for (int k = 0; k < kTK / 16; ++k) {
+          const int n = rg + 16 * k;
+          const uint4 v = *reinterpret_cast<const uint4*>(half + n * 128 + ((chunk ^ (n & 7)) << 4));
+          fs[0] += bf16lo(v.x); fs[1] += bf16hi(v.x); fs[2] += bf16lo(v.y); fs[3] += bf16hi(v.y);
+          fs[4] += bf16lo(v.z); fs[5] += bf16hi(v.z); fs[6] += bf16lo(v.w); fs[7] += bf16hi(v.w);
         }
-        csum += (double)fs;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) csum[j] += (double)fs[j];
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&empty[s]);
-      // drain the accumulator of this chunk into fp64
-      mbar_wait(&tfull[a], (i >> 1) & 1);
+      if (!last) continue;
+      // drain the window's accumulator into fp64 (four loads in flight, one wait)
+      mbar_wait(&tfull[a], (wi >> 1) & 1);
       tc::fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 128 + h * 64;
+      uint32_t r[4][16];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        uint32_t r[16];
-        tc::ld_32x32b_x16(taddr + b * 16, r);
-        tc::ld_wait();
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[b * 16 + j] += (double)__uint_as_float(r[j]);
-      }
+      for (int b = 0; b < 4; ++b) tc::ld_32x32b_x16(taddr + b * 16, r[b]);
+      tc::ld_wait();
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[a]);
-    }
-    double* out = covpart + ((size_t)u * parts + p) * kDc * kDc + (size_t)row * kDc + h * 64;
 #pragma unroll
-    for (int j = 0; j < 64; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
-    colred[thalf][cch] = csum;
+      for (int b = 0; b < 4; ++b)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[b * 16 + j] += (double)__uint_as_float(r[b][j]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) colred[rg][8 * c8 + j] = csum[j];
+    // wait for all column sums (named barrier over the 8 epilogue warps)
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (et < kDc) {
+      double s = 0.0;
+      for (int k = 0; k < 16; ++k) s += colred[k][et];
+      colsum_sm[et] = s;
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (fused) {
+      // parts == 1: this CTA saw every token of the unit -> finalize here (mu, C, C_q)
+      const double* sg = sigma + (size_t)u * kDc;
+      const double mur = center ? colsum_sm[row] / (double)N : 0.0;
+      const double sr = sg[row];
+      double* cqr = cq + (size_t)u * kDc * kDc + (size_t)row * kDc + h * 64;
+#pragma unroll
+      for (int j = 0; j < 64; j += 2) {
+        const int c0 = h * 64 + j;
+        const double m0 = center ? colsum_sm[c0] / (double)N : 0.0;
+        const double m1 = center ? colsum_sm[c0 + 1] / (double)N : 0.0;
+        const double v0 = sr * sg[c0] * (acc[j] - (double)N * mur * m0);
+        const double v1 = sr * sg[c0 + 1] * (acc[j + 1] - (double)N * mur * m1);
+        *reinterpret_cast<double2*>(cqr + j) = make_double2(v0, v1);
+      }
+      if (et < kDc) mu[(size_t)u * kDc + et] = center ? colsum_sm[et] / (double)N : 0.0;
+    } else {
+      double* out = covpart + ((size_t)u * parts + p) * kDc * kDc + (size_t)row * kDc + h * 64;
+#pragma unroll
+      for (int j = 0; j < 64; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
+      if (et < kDc) colpart[((size_t)u * parts + p) * kDc + et] = colsum_sm[et];
+    }
   }
   tc::fence_before();
   __syncthreads();
-  if (threadIdx.x < kDc)
-    colpart[((size_t)u * parts + p) * kDc + threadIdx.x] = colred[0][threadIdx.x] + colred[1][threadIdx.x];
   if (warp == 1) {
     tc::fence_after();
     tc::tmem_dealloc(tmem, 256);
@@ -197,7 +239,7 @@ bool encode_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64
 
 bool cov_tc_supported(int d, bool bf16) { return bf16 && d == kDc && get_encode() != nullptr; }
 
-int launch_cov_tc(int U, int N, const void* K, const CalibWs& ws, cudaStream_t st) {
+int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, cudaStream_t st) {
   CUtensorMap map;
   if (!encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTK, 128)) return -2;
   static bool attr = [] {
@@ -205,7 +247,9 @@ int launch_cov_tc(int U, int N, const void* K, const CalibWs& ws, cudaStream_t s
   }();
   (void)attr;
   dim3 grid(ws.parts, U);
-  cov_tc_kernel<<<grid, kThreads, kSmem, st>>>(map, N, ws.parts, ws.covpart, ws.colpart);
+  // parts == 1: the kernel also finalizes (mu, C = S - N mu mu^T, C_q) -- no finalize launch
+  cov_tc_kernel<<<grid, kThreads, kSmem, st>>>(map, N, ws.parts, ws.covpart, ws.colpart, ws.sigma, ws.cq,
+                                               ws.mu, center, ws.parts == 1);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

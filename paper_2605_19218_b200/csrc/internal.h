@@ -42,7 +42,8 @@ int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws,
 bool cov_tc_supported(int d, bool bf16);
 bool compress_tc_supported(int d, int r, bool bf16);
 int launch_compress_tc(int U, int N, int r, const void* K, const float* R, void* Kc, cudaStream_t st);
-int launch_cov_tc(int U, int N, const void* K, const CalibWs& ws, cudaStream_t st);
+// parts == 1 also finalizes (writes cq and mu): the caller skips launch_finalize
+int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, cudaStream_t st);
 int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st);
 int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st);
 int launch_select_gather(int U, int d, int r, bool fp64_vecs, bool bf16x2, bool center,
