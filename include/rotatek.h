@@ -221,6 +221,15 @@ rotatek_status rotatek_select_topr(int32_t units, int32_t head_dim, int32_t rank
 /* Number of kernel launches the last successful call on this thread enqueued. */
 int rotatek_last_launch_count(void);
 
+/*
+ * Diagnostics only (not part of the hot path): install a device buffer of
+ * >= 8 * (number of streaming warps) uint64 that subsequent decode launches of the
+ * streaming kernels fill with per-warp %globaltimer stamps (start, after the query
+ * rotation, first tile ready, loop end, end) and counters (tiles, units).  NULL
+ * uninstalls.  The buffer is caller-owned; the library keeps only the pointer.
+ */
+void rotatek_debug_decode_trace(void* device_buffer);
+
 const char* rotatek_status_string(rotatek_status status);
 const char* rotatek_last_error(void); /* thread-local detail for the last non-OK return */
 int rotatek_abi_version(void);

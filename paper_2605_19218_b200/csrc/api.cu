@@ -50,6 +50,7 @@ extern "C" {
 int rotatek_abi_version(void) { return ROTATEK_ABI_VERSION; }
 const char* rotatek_last_error(void) { return g_err; }
 int rotatek_last_launch_count(void) { return g_launches; }
+void rotatek_debug_decode_trace(void* buf) { rk::set_decode_trace(buf); }
 
 const char* rotatek_status_string(rotatek_status s) {
   switch (s) {

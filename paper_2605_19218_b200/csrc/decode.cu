@@ -14,7 +14,9 @@
 //    cut into one contiguous range per WARP; each warp streams its range through its
 //    own ring of shared-memory stages filled by 1-D TMA bulk copies
 //    (cp.async.bulk + mbarrier complete_tx, SASS UBLKCP), K~ tile then V tile, so every
-//    byte of the compacted cache is read exactly once with no CTA-level barriers.  At
+//    byte of the compacted cache is read exactly once with no CTA-level barriers.  The
+//    query rotation (q~ = q R_r, b = q . dmu) is fused: the warp that starts a unit
+//    rotates that unit's queries itself (rotate_query), so a decode is ONE launch.  At
 //    every unit boundary the warp flushes an online-softmax partial (m, l, acc[G][d]);
 //    the last warp to finish a unit (atomic ticket) merges that unit's partials in slot
 //    order (deterministic) and writes out, then re-arms the ticket (graph-replay safe).
@@ -45,55 +47,25 @@ struct DecodeParams {
   float* out;
   uint32_t* counters;
   float* partials;
-  const float* qt = nullptr;  // [U, G, r] pre-rotated, pre-scaled queries (qrot_kernel)
-  const float* qb = nullptr;  // [U, G] pre-scaled bias
+  unsigned long long* trace = nullptr;  // diagnostics: [NW][8] globaltimer stamps (or null)
+  unsigned rot = 0;                     // diagnostics: CTA -> work rotation (ROTATEK_CTA_ROT)
 };
 
-// Programmatic dependent launch: the decode kernel starts while qrot_kernel runs; only the
-// reads of q~ / b wait for it (everything the decode streams was written before qrot).
-__device__ __forceinline__ void pdl_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
 }
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// diagnostics stamp k of warp gw (lane 0 only; no-op unless a trace buffer is installed)
+#define RK_TRACE(k, v)                                                              \
+  do {                                                                              \
+    if (p.trace != nullptr && lane == 0) p.trace[(size_t)gw * 8 + (k)] = (v);       \
+  } while (0)
 
-// q~ = q R_r and b = q . dmu for every (unit, query head), pre-scaled by scale*log2(e)
-// (Alg. 2 lines 1-2; App. C P:610-616 inlines this into every program -- here it is computed
-// once per head instead of once per (head, split)).
-template <typename T>
-__global__ void __launch_bounds__(128) qrot_kernel(int G, int d, int r, const T* __restrict__ q,
-                                                   const float* __restrict__ R,
-                                                   const float* __restrict__ dmu, float sl,
-                                                   float* __restrict__ qt, float* __restrict__ qb) {
-  extern __shared__ float qsm[];  // [G][d] q, [d] dmu, then [d][r] R_r
-  float* dms = qsm + G * d;
-  float* Rs = dms + d;
-  pdl_launch_dependents();
-  const int u = blockIdx.x, tid = threadIdx.x;
-  const T* qu = q + (size_t)u * G * d;
-  const float* Ru = R + (size_t)u * d * r;
-  // one round trip: R_r (independent 16-byte loads; d*r is a multiple of 4), q and dmu
-  for (int e = tid; e < d * r / 4; e += blockDim.x)
-    reinterpret_cast<float4*>(Rs)[e] = __ldg(reinterpret_cast<const float4*>(Ru) + e);
-  for (int e = tid; e < G * d; e += blockDim.x) qsm[e] = Elem<T>::to_f(qu[e]);
-  for (int e = tid; e < d; e += blockDim.x) dms[e] = dmu ? __ldg(dmu + (size_t)u * d + e) : 0.f;
-  __syncthreads();
-  for (int e = tid; e < G * r; e += blockDim.x) {
-    const int g = e / r, k = e % r;
-    float s0 = 0.f, s1 = 0.f;
-#pragma unroll 8
-    for (int i = 0; i < d; i += 2) {
-      s0 = fmaf(qsm[g * d + i], Rs[i * r + k], s0);
-      s1 = fmaf(qsm[g * d + i + 1], Rs[(i + 1) * r + k], s1);
-    }
-    qt[((size_t)u * G + g) * r + k] = (s0 + s1) * sl;
-  }
-  const int w = tid >> 5, lane = tid & 31;
-  for (int g = w; g < G; g += blockDim.x >> 5) {
-    float s = 0.f;
-    for (int i = lane; i < d; i += 32) s = fmaf(qsm[g * d + i], dms[i], s);
-    s = warp_sum(s);
-    if (lane == 0) qb[(size_t)u * G + g] = s * sl;
-  }
+static unsigned long long* g_trace = nullptr;
+static unsigned cta_rot() {
+  const char* e = getenv("ROTATEK_CTA_ROT");
+  return e ? (unsigned)atoi(e) : 0u;
 }
 
 // =====================================================================================
@@ -286,47 +258,15 @@ size_t decode_ws_layout(int U, int G, int d, int r, int N, int M, void* base, De
   off += al256((size_t)U * 4);
   w.partials = (float*)(b ? b + off : nullptr);
   off += al256(part);
-  w.qt = (float*)(b ? b + off : nullptr);
-  off += al256((size_t)U * G * r * 4);
-  w.qb = (float*)(b ? b + off : nullptr);
-  off += al256((size_t)U * G * 4);
   w.max_splits = smax;
   if (ws) *ws = w;
   return off;
 }
 
-static bool launch_qrot(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
-  const size_t sm = ((size_t)a.G * a.d + a.d + (size_t)a.d * a.r) * sizeof(float);
-  const float sl = a.scale * kLog2e;
-  static bool attr = [] {
-    cudaFuncSetAttribute(qrot_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    cudaFuncSetAttribute(qrot_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    return true;
-  }();
-  (void)attr;
-  if (a.bf16)
-    qrot_kernel<__nv_bfloat16><<<a.U, 128, sm, st>>>(a.G, a.d, a.r, static_cast<const __nv_bfloat16*>(a.q),
-                                                     a.R, a.dmu, sl, ws.qt, ws.qb);
-  else
-    qrot_kernel<float><<<a.U, 128, sm, st>>>(a.G, a.d, a.r, static_cast<const float*>(a.q), a.R, a.dmu,
-                                             sl, ws.qt, ws.qb);
-  return cudaPeekAtLastError() == cudaSuccess;
-}
-
-// launch `kern` as a programmatic dependent of the preceding qrot_kernel
 template <typename Kern, typename... Args>
-static bool launch_pdl(Kern kern, int ctas, int threads, size_t smem, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args...) == cudaSuccess;
+static bool launch(Kern kern, int ctas, int threads, size_t smem, cudaStream_t st, Args... args) {
+  kern<<<ctas, threads, smem, st>>>(args...);
+  return cudaPeekAtLastError() == cudaSuccess;
 }
 
 template <typename T, int RK, int G, int WARPS, int STAGES, int TTV, int MINB>
@@ -345,10 +285,9 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   const FastPlan pl = fast_plan(a.U, a.N, a.M, ctas_per_sm * WARPS);
   const int ctas = (pl.NW + WARPS - 1) / WARPS;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, ws.qt, ws.qb};
-  if (!launch_qrot(a, ws, st)) return -1;
-  if (!launch_pdl(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)) return -1;
-  return 2;
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, cta_rot()};
+  if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)) return -1;
+  return 1;
 }
 
 // Default configuration per shape: 16 resident warps per SM (2 CTAs x 8 warps), one
@@ -366,9 +305,11 @@ static int launch_fast_default(const DecodeArgs& a, const DecodeWs& ws, cudaStre
                       : FastCfg<T, RK, G, 8, 1, 32>::SMEM <= 227 * 1024 ? 32 : 16;
     return launch_fast_cfg<T, RK, G, 8, 1, T64, 1>(a, ws, st);
   } else {
-    // GQA on CUDA cores: register-heavy (G accumulator sets), one CTA of 8 warps per SM
+    // GQA on CUDA cores: register-heavy (G accumulator sets), one CTA of <= 8 warps per SM
     constexpr int STG = FastCfg<T, RK, G, 8, 2, TTV>::SMEM <= 227 * 1024 ? 2 : 1;
-    return launch_fast_cfg<T, RK, G, 8, STG, TTV, 1>(a, ws, st);
+    constexpr int PER = FastCfg<T, RK, G, 1, STG, TTV>::SMEM;
+    constexpr int W = (227 * 1024) / PER < 8 ? (227 * 1024) / PER : 8;
+    return launch_fast_cfg<T, RK, G, W, STG, TTV, 1>(a, ws, st);
   }
 }
 
@@ -381,30 +322,20 @@ static int launch_fast_r32(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
     if (e && sscanf(e, "%d,%d,%d", &w, &s, &t) == 3) return w * 1000 + s * 100 + t;
     return 0;
   }();
-  if constexpr (sizeof(T) == 2) switch (cfg) {
+  if constexpr (sizeof(T) == 2 && G == 1) switch (cfg) {
     case 8132: return launch_fast_cfg<T, 32, G, 8, 1, 32, 2>(a, ws, st);
-    case 8216: return launch_fast_cfg<T, 32, G, 8, 2, 16, 2>(a, ws, st);
-    case 16132:
-      if constexpr (G == 1) return launch_fast_cfg<T, 32, G, 16, 1, 32, 1>(a, ws, st);
-      break;
-    case 16216:
-      if constexpr (G == 1) return launch_fast_cfg<T, 32, G, 16, 2, 16, 1>(a, ws, st);
-      break;
     case 8232: return launch_fast_cfg<T, 32, G, 8, 2, 32, 1>(a, ws, st);
-    case 12132: return launch_fast_cfg<T, 32, G, 12, 1, 32, 1>(a, ws, st);
-    case 8164: return launch_fast_cfg<T, 32, G, 8, 1, 64, 1>(a, ws, st);
+    case 16132: return launch_fast_cfg<T, 32, G, 16, 1, 32, 1>(a, ws, st);
     case 4264: return launch_fast_cfg<T, 32, G, 4, 2, 64, 1>(a, ws, st);
-    case 6196:
-      if constexpr (G == 1) return launch_fast_cfg<T, 32, G, 6, 1, 96, 1>(a, ws, st);
-      break;
-    case 41128:
-      if constexpr (G == 1) return launch_fast_cfg<T, 32, G, 4, 1, 128, 1>(a, ws, st);
-      break;
-    case 10148:
-      if constexpr (G == 1) return launch_fast_cfg<T, 32, G, 10, 1, 48, 1>(a, ws, st);
-      break;
+    case 41128: return launch_fast_cfg<T, 32, G, 4, 1, 128, 1>(a, ws, st);
+    case 10148: return launch_fast_cfg<T, 32, G, 10, 1, 48, 1>(a, ws, st);
     default: break;
   }
+  // short units (joint token+channel pruning, N+M <= 2048): two 32-token stages per warp
+  // keep a tile in flight across the frequent unit-boundary flushes (joint_b64: 117 vs
+  // 128 us/layer in the tools/time_decode.py sweep); long units keep one 64-token stage
+  if constexpr (sizeof(T) == 2 && G == 1)
+    if (a.N + a.M <= 2048) return launch_fast_cfg<T, 32, G, 8, 2, 32, 1>(a, ws, st);
   return launch_fast_default<T, 32, G>(a, ws, st);
 }
 
@@ -464,10 +395,9 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
   const FastPlan pl = fast_plan(a.U, a.N, a.M, WARPS);
   const int ctas = (pl.NW + WARPS - 1) / WARPS;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, ws.qt, ws.qb};
-  if (!launch_qrot(a, ws, st)) return -1;
-  if (!launch_pdl(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, pl.cmax)) return -1;
-  return 2;
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, cta_rot()};
+  if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, pl.cmax)) return -1;
+  return 1;
 }
 
 // ring configuration (ROTATEK_GQA_CFG="tile,stages" for tuning; default one 64-token stage
@@ -533,5 +463,7 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
   }
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
+
+void set_decode_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
 
 }  // namespace rk

@@ -18,6 +18,15 @@
 
 constexpr int kD = 128;
 
+// Per-unit query table entry (see rotate_unit): qt [G][RK] f32 | b [G] f32 (16-B padded) |
+// q [G][kD] in the cache dtype.
+template <typename T, int RK, int G>
+struct QEnt {
+  static constexpr int OFF_B = G * RK * 4;
+  static constexpr int OFF_Q = OFF_B + ((G + 3) / 4) * 16;
+  static constexpr int BYTES = (OFF_Q + G * kD * (int)sizeof(T) + 15) / 16 * 16;
+};
+
 template <typename T, int RK, int G, int WARPS, int STAGES, int TTV>
 struct FastCfg {
   static constexpr int S = sizeof(T);
@@ -35,11 +44,12 @@ struct FastCfg {
   static constexpr int VPL = kD / 32;                  // V channels per lane (4)
   static constexpr int NACC = (G == 1) ? 2 : 1;        // accumulator sets
   // per-warp shared memory
-  static constexpr int OFF_Q = STAGES * STAGE;                    // float [G][kD]  scaled q
-  static constexpr int OFF_QT = OFF_Q + G * kD * 4;              // float [G][RK]  scaled q~
-  static constexpr int OFF_P = OFF_QT + G * RK * 4;              // float [G][TT_P] probabilities
-  static constexpr int OFF_B = OFF_P + G * TT_P * 4;             // float [G] bias (pad 16 B)
-  static constexpr int OFF_BAR = (OFF_B + ((G + 3) / 4) * 16 + 7) / 8 * 8;
+  static constexpr int NT = (G == 1) ? 4 : 2;                    // pre-rotated units (QEnt table)
+  static constexpr int ENT = QEnt<T, RK, G>::BYTES;
+  static constexpr int OFF_Q = STAGES * STAGE;                    // float [G][kD] scaled q (G > 1)
+  static constexpr int OFF_P = OFF_Q + (G > 1 ? G * kD * 4 : 0);  // float [G][TT_P] probabilities
+  static constexpr int OFF_TAB = (OFF_P + G * TT_P * 4 + 15) / 16 * 16;  // QEnt [NT]
+  static constexpr int OFF_BAR = OFF_TAB + NT * ENT;
   static constexpr int WARP_SMEM = ((OFF_BAR + STAGES * 8) + 127) / 128 * 128;
   static constexpr int SMEM = WARPS * WARP_SMEM;
   static_assert(LPT_V >= 1 && LPT_V <= 32 && (32 % LPT_V) == 0, "bad RK");
@@ -125,11 +135,10 @@ __device__ __forceinline__ void load_v4<float>(const unsigned char* p, float* f)
 // and sits on the kernel's tail.
 template <int G>
 __device__ __forceinline__ void merge_unit(const float* __restrict__ part, int count,
-                                           float* __restrict__ out, int lane,
-                                           float* __restrict__ wsm /* >= count * G floats */) {
+                                           float* __restrict__ out, int lane) {
   constexpr int kRec = kD + 4;
-  // pass 1 (lanes over slots): per-head max of m, then the slot weights 2^(m_s - max) into
-  // shared memory and the merged denominator sum_s l_s 2^(m_s - max)
+  // pass 1 (lanes over slots): per-head max of m and the merged denominator
+  // sum_s l_s 2^(m_s - max)
   float mloc[G];
 #pragma unroll
   for (int g = 0; g < G; ++g) mloc[g] = -CUDART_INF_F;
@@ -148,13 +157,12 @@ __device__ __forceinline__ void merge_unit(const float* __restrict__ part, int c
       const float* src = part + ((size_t)s * G + g) * kRec;
       const float ms = __ldcg(src + kD);
       const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - mloc[g]);
-      wsm[s * G + g] = f;
       Ls[g] = fmaf(__ldcg(src + kD + 1), f, Ls[g]);
     }
 #pragma unroll
   for (int g = 0; g < G; ++g) Ls[g] = warp_sum(Ls[g]);
-  __syncwarp();
-  // pass 2 (lanes over channels): weighted sum of the accumulators, 4 slots in flight
+  // pass 2 (lanes over channels): weighted sum of the accumulators; the slot weight is
+  // recomputed from the (uniform) m_s load exactly as in pass 1
   float A[G][4];
 #pragma unroll
   for (int g = 0; g < G; ++g) A[g][0] = A[g][1] = A[g][2] = A[g][3] = 0.f;
@@ -162,19 +170,153 @@ __device__ __forceinline__ void merge_unit(const float* __restrict__ part, int c
   for (int s = 0; s < count; ++s) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
-      const float4 v = __ldcg(reinterpret_cast<const float4*>(part + ((size_t)s * G + g) * kRec + lane * 4));
-      const float f = wsm[s * G + g];
+      const float* src = part + ((size_t)s * G + g) * kRec;
+      const float4 v = __ldcg(reinterpret_cast<const float4*>(src + lane * 4));
+      const float ms = __ldcg(src + kD);
+      const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - mloc[g]);
       A[g][0] = fmaf(v.x, f, A[g][0]); A[g][1] = fmaf(v.y, f, A[g][1]);
       A[g][2] = fmaf(v.z, f, A[g][2]); A[g][3] = fmaf(v.w, f, A[g][3]);
     }
   }
-  __syncwarp();
 #pragma unroll
   for (int g = 0; g < G; ++g) {
     const float inv = 1.f / Ls[g];
     *reinterpret_cast<float4*>(out + (size_t)g * kD + lane * 4) =
         make_float4(A[g][0] * inv, A[g][1] * inv, A[g][2] * inv, A[g][3] * inv);
   }
+}
+
+// Query rotation fused into the decode (Alg. 2 l.1-2; App. C, index reading Q14):
+//   q~[g][k] = sum_i q[g][i] R_r[i][k],   b[g] = q[g] . dmu,
+// pre-multiplied by scale*log2(e), for the G query heads of one unit.  There is no separate
+// pre-rotation launch: every warp rotates the (few) units its token range touches into a
+// warp-private table BEFORE it issues its first tile load, i.e. while the memory system is
+// still idle -- every operand (q, dmu, R_r as float4 rows) is one independent load, so the
+// whole rotation costs one round trip.  Rotating after the first loads were issued would
+// queue these dependent reads behind the whole-GPU tile burst (measured: +17 us/launch).
+// Table entry (QEnt): qt [G][RK] f32 | b [G] f32 (16-B padded) | q [G][kD] raw dtype.
+
+template <typename T>
+__device__ __forceinline__ void unpack16(const unsigned char* p, float* f);  // 16 bytes
+template <>
+__device__ __forceinline__ void unpack16<__nv_bfloat16>(const unsigned char* p, float* f) {
+  const uint4 a = *reinterpret_cast<const uint4*>(p);
+  const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) { f[2 * i] = bf16lo(w[i]); f[2 * i + 1] = bf16hi(w[i]); }
+}
+template <>
+__device__ __forceinline__ void unpack16<float>(const unsigned char* p, float* f) {
+  const float4 a = *reinterpret_cast<const float4*>(p);
+  f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
+}
+
+template <typename T, int RK, int G>
+__device__ __forceinline__ void rotate_unit(const DecodeParams& p, int u, int lane, unsigned char* ent) {
+  using E = QEnt<T, RK, G>;
+  static_assert(RK % 4 == 0 && RK <= 128 && 128 % RK == 0, "rank");
+  constexpr int S = sizeof(T);
+  constexpr int QCH = G * kD * S / 16;       // 16-byte chunks of q
+  constexpr int QPL = (QCH + 31) / 32;       // ... per lane
+  constexpr int C4 = RK / 4;                 // float4 column blocks of an R_r row
+  constexpr int NR = kD * C4 / 32;           // rows per lane: row group r0 owns rows [r0*NR, r0*NR+NR)
+  constexpr int BATCH = NR < 32 ? NR : 32;   // rows per load batch (one round trip)
+  constexpr int QV = 16 / S;                 // q values per 16-byte shared-memory read
+  const int j = lane % C4, r0 = lane / C4;
+  const float4* Rr = reinterpret_cast<const float4*>(p.R + (size_t)u * kD * RK) + (size_t)r0 * NR * C4 + j;
+  const uint4* qsrc = reinterpret_cast<const uint4*>(static_cast<const T*>(p.q) + (size_t)u * G * kD);
+  // all loads of the first batch are independent: one round trip
+  float4 rv[BATCH];
+#pragma unroll
+  for (int t = 0; t < BATCH; ++t) rv[t] = __ldg(Rr + (size_t)t * C4);
+  uint4 qv[QPL];
+#pragma unroll
+  for (int t = 0; t < QPL; ++t)
+    if (lane + 32 * t < QCH) qv[t] = __ldg(qsrc + lane + 32 * t);
+  const float4 dm = p.dmu ? __ldg(reinterpret_cast<const float4*>(p.dmu + (size_t)u * kD) + lane)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+  __syncwarp();  // previous readers of this entry are done
+  uint4* qdst = reinterpret_cast<uint4*>(ent + E::OFF_Q);
+#pragma unroll
+  for (int t = 0; t < QPL; ++t)
+    if (lane + 32 * t < QCH) qdst[lane + 32 * t] = qv[t];
+  __syncwarp();
+  const T* qe = reinterpret_cast<const T*>(ent + E::OFF_Q);
+  float* be = reinterpret_cast<float*>(ent + E::OFF_B);
+  // b = q . dmu (lane owns channels 4*lane .. 4*lane+3)
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const T* qg = qe + g * kD + 4 * lane;
+    float sb = Elem<T>::to_f(qg[0]) * dm.x;
+    sb = fmaf(Elem<T>::to_f(qg[1]), dm.y, sb);
+    sb = fmaf(Elem<T>::to_f(qg[2]), dm.z, sb);
+    sb = fmaf(Elem<T>::to_f(qg[3]), dm.w, sb);
+    sb = warp_sum(sb);
+    if (lane == 0) be[g] = sb * p.sl;
+  }
+  // q~: lane accumulates columns 4j..4j+3 over its contiguous row block; q rows are read
+  // 16 bytes at a time from the entry
+  float acc[G][4];
+#pragma unroll
+  for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
+  const unsigned char* qrow0 = ent + E::OFF_Q + (size_t)r0 * NR * S;
+#pragma unroll
+  for (int s0 = 0; s0 < NR; s0 += BATCH) {
+    if (s0 > 0) {
+#pragma unroll
+      for (int t = 0; t < BATCH; ++t) rv[t] = __ldg(Rr + (size_t)(s0 + t) * C4);
+    }
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+#pragma unroll
+      for (int v = 0; v < BATCH / QV; ++v) {
+        float qf[QV];
+        unpack16<T>(qrow0 + ((size_t)g * kD + s0 + v * QV) * S, qf);
+#pragma unroll
+        for (int e = 0; e < QV; ++e) {
+          const float4 r4 = rv[v * QV + e];
+          acc[g][0] = fmaf(qf[e], r4.x, acc[g][0]);
+          acc[g][1] = fmaf(qf[e], r4.y, acc[g][1]);
+          acc[g][2] = fmaf(qf[e], r4.z, acc[g][2]);
+          acc[g][3] = fmaf(qf[e], r4.w, acc[g][3]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = C4; o < 32; o <<= 1)
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[g][k] += __shfl_xor_sync(0xffffffffu, acc[g][k], o);
+  if (lane < C4) {
+    float* qt = reinterpret_cast<float*>(ent);
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+      *reinterpret_cast<float4*>(qt + g * RK + 4 * j) =
+          make_float4(acc[g][0] * p.sl, acc[g][1] * p.sl, acc[g][2] * p.sl, acc[g][3] * p.sl);
+  }
+  __syncwarp();
+}
+
+// Pre-rotate the first NT units of the token range [a, b) into the table (kernel start).
+template <typename T, int RK, int G, int NT, int ENT>
+__device__ __forceinline__ void prerotate(const DecodeParams& p, long long a, long long b, long long L,
+                                          int lane, unsigned char* tab) {
+  const int ua = (int)(a / L), ub = (int)((b - 1) / L);
+  const int n = ub - ua + 1 < NT ? ub - ua + 1 : NT;
+  for (int k = 0; k < n; ++k) rotate_unit<T, RK, G>(p, ua + k, lane, tab + k * ENT);
+}
+
+// Table entry of unit u for a warp whose range starts in unit ua (rotates lazily when the
+// range touches more than NT units; the slot's previous unit is finished by then).
+template <typename T, int RK, int G, int NT, int ENT>
+__device__ __forceinline__ unsigned char* unit_entry(const DecodeParams& p, int u, int ua, int lane,
+                                                     unsigned char* tab) {
+  const int k = u - ua;
+  unsigned char* ent = tab + (k % NT) * ENT;
+  if (k >= NT) rotate_unit<T, RK, G>(p, u, lane, ent);
+  return ent;
 }
 
 // One tile: scores (key rows of KR channels), online-softmax rescale, P.V.
@@ -291,13 +433,12 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   constexpr int NACC = C::NACC;
   extern __shared__ __align__(128) unsigned char fsm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * WARPS + w;
+  const int gw = (int)((blockIdx.x + p.rot) % gridDim.x) * WARPS + w;
   if (gw >= NW) return;
   unsigned char* base = fsm + w * C::WARP_SMEM;
   float* qs = reinterpret_cast<float*>(base + C::OFF_Q);
-  float* qts = reinterpret_cast<float*>(base + C::OFF_QT);
   float* pbuf = reinterpret_cast<float*>(base + C::OFF_P);
-  float* bs = reinterpret_cast<float*>(base + C::OFF_B);
+  unsigned char* tab = base + C::OFF_TAB;
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
 
   const int N = p.N, M = p.M;
@@ -317,6 +458,10 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
     fence_mbar_init();
   }
   __syncwarp();
+  RK_TRACE(0, gtime());
+  const int ua = (int)(a / L);
+  prerotate<T, RK, G, C::NT, C::ENT>(p, a, b, L, lane, tab);
+  RK_TRACE(1, gtime());
 
   // ---------------- producer (lane 0): issue the tile at cursor px into stage st
   long long px = a;
@@ -344,32 +489,23 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   float qreg[C::CHN], xreg[C::CHN];  // register copies of q~ / q chunks when G == 1
   int cur_u = -1;
 
-  pdl_wait();  // q~ and b come from qrot_kernel (programmatic dependent launch)
+  const float* qts = nullptr;  // current unit's scaled q~ [G][RK] and bias [G] (table entry)
+  const float* bs = nullptr;
   auto setup = [&](int u) {
-    // scaled q (text keys), q~ = q R_r and b = q . dmu precomputed by qrot_kernel
-    const T* qg = static_cast<const T*>(p.q) + (size_t)u * G * kD;
+    const unsigned char* ent = unit_entry<T, RK, G, C::NT, C::ENT>(p, u, ua, lane, tab);
+    using E = QEnt<T, RK, G>;
+    qts = reinterpret_cast<const float*>(ent);
+    bs = reinterpret_cast<const float*>(ent + E::OFF_B);
+    const T* qe = reinterpret_cast<const T*>(ent + E::OFF_Q);
     if constexpr (G == 1) {
-      // register chunks straight from global memory (independent 16-byte loads)
       const int cv = lane % C::LPT_V, cx = lane % C::LPT_X;
-      const float4* t4 = reinterpret_cast<const float4*>(p.qt + (size_t)u * RK + cv * C::CHN);
-      float4 tv[C::CHN / 4];
 #pragma unroll
-      for (int i = 0; i < C::CHN / 4; ++i) tv[i] = __ldcg(t4 + i);
-      float xf[C::CHN];
-      unpack_chunk<T>(reinterpret_cast<const unsigned char*>(qg + cx * C::CHN), xf);
-      const float bq = __ldcg(p.qb + u);
-#pragma unroll
-      for (int i = 0; i < C::CHN / 4; ++i) {
-        qreg[4 * i] = tv[i].x; qreg[4 * i + 1] = tv[i].y; qreg[4 * i + 2] = tv[i].z; qreg[4 * i + 3] = tv[i].w;
+      for (int i = 0; i < C::CHN; ++i) {
+        qreg[i] = qts[cv * C::CHN + i];
+        xreg[i] = Elem<T>::to_f(qe[cx * C::CHN + i]) * p.sl;
       }
-#pragma unroll
-      for (int i = 0; i < C::CHN; ++i) xreg[i] = xf[i] * p.sl;
-      if (lane == 0) bs[0] = bq;
-      __syncwarp();
     } else {
-      for (int e = lane; e < G * kD; e += 32) qs[e] = Elem<T>::to_f(qg[e]) * p.sl;
-      for (int e = lane; e < G * RK; e += 32) qts[e] = __ldcg(p.qt + (size_t)u * G * RK + e);
-      if (lane < G) bs[lane] = __ldcg(p.qb + (size_t)u * G + lane);
+      for (int e = lane; e < G * kD; e += 32) qs[e] = Elem<T>::to_f(qe[e]) * p.sl;
       __syncwarp();
     }
 #pragma unroll
@@ -383,6 +519,19 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
     }
   };
 
+  // the last arrival at a unit's ticket merges its partials (deferring the first unit's
+  // arrival to the end of the range was measured slower: it serialises two merges in the
+  // tail)
+  auto arrive = [&](int u, int count) {
+    constexpr int kRec = kD + 4;
+    __syncwarp();
+    unsigned prev = 0;
+    if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != (unsigned)(count - 1)) return;
+    merge_unit<G>(p.partials + ((size_t)u * cmax) * G * kRec, count, p.out + (size_t)u * G * kD, lane);
+    if (lane == 0) p.counters[u] = 0u;
+  };
   auto flush = [&](int u) {
     const long long x0 = (long long)u * L, x1 = x0 + L - 1;
     const int first = warp_of(x0, Ttot, NW), last = warp_of(x1, Ttot, NW);
@@ -417,13 +566,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
       if (lane == 0) { dst[kD] = m[g]; dst[kD + 1] = lt[g]; }
       *reinterpret_cast<float4*>(dst + lane * 4) = make_float4(A[g][0], A[g][1], A[g][2], A[g][3]);
     }
-    __syncwarp();
-    unsigned prev = 0;
-    if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], 1u);
-    prev = __shfl_sync(0xffffffffu, prev, 0);
-    if (prev != (unsigned)(count - 1)) return;
-    merge_unit<G>(part, count, p.out + (size_t)u * G * kD, lane, qs);  // qs is free until setup
-    if (lane == 0) p.counters[u] = 0u;
+    arrive(u, count);
   };
 
   // ---------------- main loop over this warp's tiles
@@ -439,6 +582,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
       cur_u = tl.u;
     }
     mbar_wait(&bar[st], ph);
+    if (j == 0) RK_TRACE(2, gtime());
     const unsigned char* kbuf = base + st * C::STAGE;
     if (tl.vis) {
       const unsigned char* vbuf = kbuf + C::TT_V * RK * C::S;
@@ -465,5 +609,14 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
     cx += tl.tn;
     ++j;
   }
+  RK_TRACE(3, gtime());
   if (cur_u >= 0) flush(cur_u);
+  RK_TRACE(4, gtime());
+  RK_TRACE(5, (unsigned long long)j);
+  RK_TRACE(6, (unsigned long long)(cur_u - ua + 1));
+  if (p.trace != nullptr && lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    RK_TRACE(7, (unsigned long long)smid);
+  }
 }

@@ -64,10 +64,10 @@ struct GqaCfg {
   static constexpr int TX = (STAGE / 512) / 16 * 16;  // text tile tokens (4 halves fit a stage)
   static constexpr int XH = TX * 128;               // one 64-channel text half
   static constexpr int NSTG = STAGES;
-  static constexpr int OFF_Q = NSTG * STAGE;                   // float [G][128] (merge scratch)
-  static constexpr int OFF_QT = OFF_Q + G * 128 * 4;           // float [G][RK]
-  static constexpr int OFF_B = OFF_QT + G * RK * 4;            // float [8]
-  static constexpr int OFF_BAR = OFF_B + 32;
+  static constexpr int NT = 2;                                 // pre-rotated units
+  static constexpr int ENT = QEnt<__nv_bfloat16, RK, G>::BYTES;
+  static constexpr int OFF_TAB = NSTG * STAGE;                 // QEnt [NT]
+  static constexpr int OFF_BAR = OFF_TAB + NT * ENT;
   static constexpr int WARP_SMEM = (OFF_BAR + 8 * NSTG + 1023) / 1024 * 1024;
   static constexpr int SMEM = WARPS * WARP_SMEM + 1024;        // + alignment slack
   static_assert(STAGE >= 4 * XH && TX >= 16, "text tile must fit the stage");
@@ -88,12 +88,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   extern __shared__ unsigned char gsm_raw[];
   unsigned char* gsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * WARPS + w;
+  const int gw = (int)((blockIdx.x + p.rot) % gridDim.x) * WARPS + w;
   if (gw >= NW) return;
   unsigned char* base = gsm + w * C::WARP_SMEM;
-  float* qs = reinterpret_cast<float*>(base + C::OFF_Q);
-  float* qts = reinterpret_cast<float*>(base + C::OFF_QT);
-  float* bs = reinterpret_cast<float*>(base + C::OFF_B);
+  unsigned char* tab = base + C::OFF_TAB;
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
   const uint32_t sbase = smem_u32(base);
 
@@ -102,6 +100,10 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   const long long Ttot = L * p.U;
   const long long a = range_start(Ttot, gw, NW), b = range_start(Ttot, gw + 1, NW);
   if (a >= b) return;
+  RK_TRACE(0, gtime());
+  const int ua = (int)(a / L);
+  prerotate<__nv_bfloat16, RK, G, C::NT, C::ENT>(p, a, b, L, lane, tab);  // before any tile load
+  RK_TRACE(1, gtime());
   const uint64_t pol = policy_evict_first();
   if (lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
@@ -146,27 +148,31 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   float acc[16][4];
   int cur_u = -1;
 
-  pdl_wait();  // q~ and b come from qrot_kernel (programmatic dependent launch)
   auto setup = [&](int u) {
+    // q~ = q R_r, b = q . dmu and q of the unit's G heads from the warp's rotation table
+    using E = QEnt<__nv_bfloat16, RK, G>;
+    const unsigned char* ent = unit_entry<__nv_bfloat16, RK, G, C::NT, C::ENT>(p, u, ua, lane, tab);
+    const float* qts = reinterpret_cast<const float*>(ent);
+    const float* bs = reinterpret_cast<const float*>(ent + E::OFF_B);
     // A fragments straight from global memory (all loads independent): row g holds the
     // bf16 "hi" part, row g + 8 the "lo" remainder; k columns 2c, 2c+1 and 8+2c, 9+2c.
     const int gl = live ? g : 0;
-    const float2* t2 = reinterpret_cast<const float2*>(p.qt + ((size_t)u * G + gl) * RK);
+    const float2* t2 = reinterpret_cast<const float2*>(qts + gl * RK);
     const __nv_bfloat162* q2 =
-        reinterpret_cast<const __nv_bfloat162*>(static_cast<const __nv_bfloat16*>(p.q) + ((size_t)u * G + gl) * kD);
+        reinterpret_cast<const __nv_bfloat162*>(ent + E::OFF_Q) + gl * (kD / 2);
     float2 tq[NKS][2];
     __nv_bfloat162 xq[8][2];
 #pragma unroll
     for (int kk = 0; kk < NKS; ++kk) {
-      tq[kk][0] = __ldcg(t2 + 8 * kk + c);
-      tq[kk][1] = __ldcg(t2 + 8 * kk + 4 + c);
+      tq[kk][0] = t2[8 * kk + c];
+      tq[kk][1] = t2[8 * kk + 4 + c];
     }
 #pragma unroll
     for (int kk = 0; kk < 8; ++kk) {
       xq[kk][0] = q2[8 * kk + c];
       xq[kk][1] = q2[8 * kk + 4 + c];
     }
-    const float bq = __ldcg(p.qb + (size_t)u * G + gl);
+    const float bq = bs[gl];
     const float z = live ? 1.f : 0.f;
 #pragma unroll
     for (int kk = 0; kk < NKS; ++kk) {
@@ -230,6 +236,17 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     }
   };
 
+  // the last arrival at a unit's ticket merges its partials
+  auto arrive = [&](int u, int count) {
+    constexpr int kRec = kD + 4;
+    __syncwarp();
+    unsigned prev = 0;
+    if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], 1u);
+    prev = __shfl_sync(0xffffffffu, prev, 0);
+    if (prev != (unsigned)(count - 1)) return;
+    merge_unit<G>(p.partials + ((size_t)u * cmax) * G * kRec, count, p.out + (size_t)u * G * kD, lane);
+    if (lane == 0) p.counters[u] = 0u;
+  };
   auto flush = [&](int u) {
     const long long x0 = (long long)u * L, x1 = x0 + L - 1;
     const int first = warp_of(x0, Ttot, NW), last = warp_of(x1, Ttot, NW);
@@ -257,13 +274,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
         *reinterpret_cast<float2*>(dst + 8 * j + 2 * c) = make_float2(acc[j][0] + acc[j][2], acc[j][1] + acc[j][3]);
       if (c == 0) { dst[kD] = m; dst[kD + 1] = lt; }
     }
-    __syncwarp();
-    unsigned prev = 0;
-    if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], 1u);
-    prev = __shfl_sync(0xffffffffu, prev, 0);
-    if (prev != (unsigned)(count - 1)) return;
-    merge_unit<G>(part, count, p.out + (size_t)u * G * kD, lane, qs);  // qs is free until setup
-    if (lane == 0) p.counters[u] = 0u;
+    arrive(u, count);
   };
 
   using NbV = std::integral_constant<int, C::TT / 8>;
@@ -280,6 +291,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     }
     const int st = j % STAGES;
     mbar_wait(&bar[st], (uint32_t)((j / STAGES) & 1));
+    if (j == 0) RK_TRACE(2, gtime());
     const uint32_t sb = sbase + st * C::STAGE;
     const int mid = lane >> 3, r8 = lane & 7;
     if (tl.vis) {
@@ -328,5 +340,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     cx += tl.tn;
     ++j;
   }
+  RK_TRACE(3, gtime());
   if (cur_u >= 0) flush(cur_u);
+  RK_TRACE(4, gtime());
+  RK_TRACE(5, (unsigned long long)j);
+  RK_TRACE(6, (unsigned long long)(cur_u - ua + 1));
+  if (p.trace != nullptr && lane == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    RK_TRACE(7, (unsigned long long)smid);
+  }
 }

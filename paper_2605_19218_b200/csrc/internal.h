@@ -25,8 +25,6 @@ struct CalibWs {
 struct DecodeWs {
   uint32_t* counters;  // [U] zero on entry, left zero
   float* partials;     // [U, G, S, d + 2] (generic) or [U, cmax, G, d + 4] (streaming)
-  float* qt;           // [U, G, r]  q~ = q R_r * scale * log2(e)   (written by qrot_kernel)
-  float* qb;           // [U, G]     b  = q . dmu * scale * log2(e)
   int max_splits;
 };
 
@@ -71,6 +69,7 @@ struct DecodeArgs {
   float* out;
 };
 // kernel: 0 auto, 1 generic, 2 fast.  Returns launches, -1 launch error, -2 unsupported.
+void set_decode_trace(void* buf);  // diagnostics (rotatek_debug_decode_trace)
 int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kernel,
                   cudaStream_t st);
 

@@ -78,6 +78,8 @@ def lib():
             L.rotatek_last_error.restype = ctypes.c_char_p
             L.rotatek_abi_version.restype = ctypes.c_int
             L.rotatek_last_launch_count.restype = ctypes.c_int
+            L.rotatek_debug_decode_trace.argtypes = [vp]
+            L.rotatek_debug_decode_trace.restype = None
             _lib = L
     return _lib
 
@@ -91,6 +93,12 @@ def _check(status: int):
 
 def last_launch_count() -> int:
     return lib().rotatek_last_launch_count()
+
+
+def debug_decode_trace(buf: torch.Tensor | None):
+    """Diagnostics: per-warp globaltimer stamps of the streaming decode kernels into
+    buf (int64 device tensor of >= 8 * warps), or None to uninstall."""
+    lib().rotatek_debug_decode_trace(None if buf is None else ctypes.c_void_p(buf.data_ptr()))
 
 
 def _dtype_code(t: torch.Tensor) -> int:
