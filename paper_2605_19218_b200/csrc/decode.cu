@@ -48,7 +48,7 @@ struct DecodeParams {
   uint32_t* counters;
   float* partials;
   unsigned long long* trace = nullptr;  // diagnostics: [NW][8] globaltimer stamps (or null)
-  unsigned rot = 0;                     // diagnostics: CTA -> work rotation (ROTATEK_CTA_ROT)
+  int aw = 0;                           // active (streaming) warps per CTA (<= WARPS)
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -59,13 +59,24 @@ __device__ __forceinline__ unsigned long long gtime() {
 // diagnostics stamp k of warp gw (lane 0 only; no-op unless a trace buffer is installed)
 #define RK_TRACE(k, v)                                                              \
   do {                                                                              \
-    if (p.trace != nullptr && lane == 0) p.trace[(size_t)gw * 8 + (k)] = (v);       \
+    if (p.trace != nullptr && lane == 0 && w < p.aw) p.trace[(size_t)gw * 8 + (k)] = (v); \
   } while (0)
 
 static unsigned long long* g_trace = nullptr;
-static unsigned cta_rot() {
-  const char* e = getenv("ROTATEK_CTA_ROT");
-  return e ? (unsigned)atoi(e) : 0u;
+
+// max units one CTA's token range can touch (its query table must hold them all)
+static int cta_units_max(int U, int N, int M, int NW, int warps) {
+  const long long L = (long long)N + M, T = L * U;
+  const long long per = (T + NW - 1) / NW + 1;  // >= any warp's range length
+  long long n = (per * warps + L - 2) / L + 1;
+  return n > U ? U : (int)n;
+}
+// streaming warps per CTA such that one CTA's units fit its query table (tiny units only
+// lower it below WARPS); 0 if even one warp's range touches more than cap units
+static int active_warps(int U, int N, int M, int NW, int warps, int cap) {
+  for (int aw = warps; aw >= 1; --aw)
+    if (cta_units_max(U, N, M, NW, aw) <= cap) return aw;
+  return 0;
 }
 
 // =====================================================================================
@@ -283,9 +294,11 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
     return n < 1 ? 1 : n;
   }();
   const FastPlan pl = fast_plan(a.U, a.N, a.M, ctas_per_sm * WARPS);
-  const int ctas = (pl.NW + WARPS - 1) / WARPS;
+  const int aw = active_warps(a.U, a.N, a.M, pl.NW, WARPS, C::CAP);
+  if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
+  const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, cta_rot()};
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw};
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)) return -1;
   return 1;
 }
@@ -370,8 +383,9 @@ static bool fast_supported(const DecodeArgs& a) {
 // ------------------------------------------------------------- tensor-core GQA launcher
 template <int RK, int G, int TTV, int STAGES, int MAXW>
 constexpr int gqa_warps() {
-  constexpr int per = GqaCfg<RK, G, 1, TTV, STAGES>::WARP_SMEM;
-  constexpr int w = (227 * 1024 - 1024) / per;
+  using C1 = GqaCfg<RK, G, 1, TTV, STAGES>;
+  constexpr int per = C1::WARP_SMEM;
+  constexpr int w = (227 * 1024 - 1024 - C1::CAP * C1::ENT) / per;
   return w > MAXW ? MAXW : w;
 }
 
@@ -393,9 +407,11 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
   }();
   (void)attr;
   const FastPlan pl = fast_plan(a.U, a.N, a.M, WARPS);
-  const int ctas = (pl.NW + WARPS - 1) / WARPS;
+  const int aw = active_warps(a.U, a.N, a.M, pl.NW, WARPS, C::CAP);
+  if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
+  const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, cta_rot()};
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw};
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, pl.cmax)) return -1;
   return 1;
 }
@@ -441,11 +457,16 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
   const bool fast_ok = fast_supported(a);
   const bool gqa_ok = gqa_supported(a);
   if ((kernel == 2 && !fast_ok) || (kernel == 3 && !gqa_ok)) return -2;
+  // -3: the streaming kernels' CTA query table cannot hold the units of one CTA range
+  // (tiny units, e.g. N + M < ~100 tokens); the generic kernel handles those shapes
   if (kernel == 3 || (kernel == 0 && gqa_ok && splits <= 0)) {
-    return a.r == 32 ? launch_gqa_rk<32>(a, ws, st) : launch_gqa_rk<64>(a, ws, st);
-  }
-  if ((kernel == 0 && fast_ok && splits <= 0) || kernel == 2) {
-    return a.bf16 ? launch_fast_rk<__nv_bfloat16>(a, ws, st) : launch_fast_rk<float>(a, ws, st);
+    const int rc = a.r == 32 ? launch_gqa_rk<32>(a, ws, st) : launch_gqa_rk<64>(a, ws, st);
+    if (rc != -3) return rc;
+    if (kernel == 3) return -2;
+  } else if ((kernel == 0 && fast_ok && splits <= 0) || kernel == 2) {
+    const int rc = a.bf16 ? launch_fast_rk<__nv_bfloat16>(a, ws, st) : launch_fast_rk<float>(a, ws, st);
+    if (rc != -3) return rc;
+    if (kernel == 2) return -2;
   }
   int S = splits > 0 ? splits : decode_max_splits(a.U, a.N, a.M);
   if (S > ws.max_splits) S = ws.max_splits;

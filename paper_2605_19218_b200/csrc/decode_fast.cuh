@@ -44,14 +44,15 @@ struct FastCfg {
   static constexpr int VPL = kD / 32;                  // V channels per lane (4)
   static constexpr int NACC = (G == 1) ? 2 : 1;        // accumulator sets
   // per-warp shared memory
-  static constexpr int NT = (G == 1) ? 4 : 2;                    // pre-rotated units (QEnt table)
-  static constexpr int ENT = QEnt<T, RK, G>::BYTES;
   static constexpr int OFF_Q = STAGES * STAGE;                    // float [G][kD] scaled q (G > 1)
   static constexpr int OFF_P = OFF_Q + (G > 1 ? G * kD * 4 : 0);  // float [G][TT_P] probabilities
-  static constexpr int OFF_TAB = (OFF_P + G * TT_P * 4 + 15) / 16 * 16;  // QEnt [NT]
-  static constexpr int OFF_BAR = OFF_TAB + NT * ENT;
+  static constexpr int OFF_BAR = (OFF_P + G * TT_P * 4 + 7) / 8 * 8;
   static constexpr int WARP_SMEM = ((OFF_BAR + STAGES * 8) + 127) / 128 * 128;
-  static constexpr int SMEM = WARPS * WARP_SMEM;
+  // CTA-shared query table: one QEnt per unit the CTA's token range touches
+  static constexpr int CAP = (G == 1) ? 32 : 8;
+  static constexpr int ENT = QEnt<T, RK, G>::BYTES;
+  static constexpr int OFF_TAB = WARPS * WARP_SMEM;
+  static constexpr int SMEM = OFF_TAB + CAP * ENT;
   static_assert(LPT_V >= 1 && LPT_V <= 32 && (32 % LPT_V) == 0, "bad RK");
   static_assert(TT_X >= XQ && TT_X % 4 == 0, "text tile too small");
   static_assert(TT_V % TPS_V == 0 && TT_V % 4 == 0, "tile");
@@ -188,14 +189,14 @@ __device__ __forceinline__ void merge_unit(const float* __restrict__ part, int c
 
 // Query rotation fused into the decode (Alg. 2 l.1-2; App. C, index reading Q14):
 //   q~[g][k] = sum_i q[g][i] R_r[i][k],   b[g] = q[g] . dmu,
-// pre-multiplied by scale*log2(e), for the G query heads of one unit.  There is no separate
-// pre-rotation launch: every warp rotates the (few) units its token range touches into a
-// warp-private table BEFORE it issues its first tile load, i.e. while the memory system is
-// still idle -- every operand (q, dmu, R_r as float4 rows) is one independent load, so the
-// whole rotation costs one round trip.  Rotating after the first loads were issued would
-// queue these dependent reads behind the whole-GPU tile burst (measured: +17 us/launch).
+// pre-multiplied by scale*log2(e).  There is no separate pre-rotation launch: at kernel
+// start the warps of a CTA rotate, together, every unit the CTA's token range touches into
+// a CTA-shared table (rotate_cta), BEFORE any tile load is issued -- every operand (q, dmu,
+// R_r rows as float4) is one independent load, so the rotation costs one round trip on an
+// idle memory system.  Rotating after the first tile loads were issued queues these reads
+// behind the whole-GPU tile burst (measured: +17 us/launch); one warp rotating all G = 7
+// heads of its unit alone took 4 us of FMA (measured), split over the CTA it is ~4x less.
 // Table entry (QEnt): qt [G][RK] f32 | b [G] f32 (16-B padded) | q [G][kD] raw dtype.
-
 template <typename T>
 __device__ __forceinline__ void unpack16(const unsigned char* p, float* f);  // 16 bytes
 template <>
@@ -211,67 +212,68 @@ __device__ __forceinline__ void unpack16<float>(const unsigned char* p, float* f
   f[0] = a.x; f[1] = a.y; f[2] = a.z; f[3] = a.w;
 }
 
-template <typename T, int RK, int G>
-__device__ __forceinline__ void rotate_unit(const DecodeParams& p, int u, int lane, unsigned char* ent) {
+// Columns [cb*CW, cb*CW + CW) of q~ (all G heads) of unit u into its table entry (one warp);
+// the cb == 0 warp also stores the raw q rows and b = q . dmu.  Lane (j, r0) owns the
+// float4 column block j over a contiguous block of NR rows; every operand is one
+// independent load (R_r rows as float4, q rows as 16-byte chunks straight from global
+// memory), so an item costs one round trip.  Splitting a unit by columns rather than by
+// heads keeps each R_r byte read once per CTA (head splitting re-read it per warp and made
+// G = 7 rotation 4 us, measured).
+template <typename T, int RK, int CW, int G>
+__device__ __forceinline__ void rotate_cols(const DecodeParams& p, int u, int cb, int lane,
+                                            unsigned char* ent) {
   using E = QEnt<T, RK, G>;
-  static_assert(RK % 4 == 0 && RK <= 128 && 128 % RK == 0, "rank");
   constexpr int S = sizeof(T);
-  constexpr int QCH = G * kD * S / 16;       // 16-byte chunks of q
-  constexpr int QPL = (QCH + 31) / 32;       // ... per lane
-  constexpr int C4 = RK / 4;                 // float4 column blocks of an R_r row
-  constexpr int NR = kD * C4 / 32;           // rows per lane: row group r0 owns rows [r0*NR, r0*NR+NR)
-  constexpr int BATCH = NR < 32 ? NR : 32;   // rows per load batch (one round trip)
-  constexpr int QV = 16 / S;                 // q values per 16-byte shared-memory read
+  constexpr int C4 = CW / 4;                 // float4 column blocks of the item
+  static_assert(C4 >= 1 && C4 <= 32 && 32 % C4 == 0 && RK % CW == 0, "columns");
+  constexpr int NR = kD * C4 / 32;           // rows per lane
+  constexpr int QV = 16 / S;                 // q values per 16-byte chunk
+  static_assert(NR % QV == 0, "row block");
+  constexpr int BATCH = NR < 32 ? NR : 32;
   const int j = lane % C4, r0 = lane / C4;
-  const float4* Rr = reinterpret_cast<const float4*>(p.R + (size_t)u * kD * RK) + (size_t)r0 * NR * C4 + j;
-  const uint4* qsrc = reinterpret_cast<const uint4*>(static_cast<const T*>(p.q) + (size_t)u * G * kD);
-  // all loads of the first batch are independent: one round trip
+  const float4* Rr = reinterpret_cast<const float4*>(p.R + (size_t)u * kD * RK + (size_t)r0 * NR * RK +
+                                                     cb * CW) + j;
+  const T* qu = static_cast<const T*>(p.q) + (size_t)u * G * kD;
   float4 rv[BATCH];
 #pragma unroll
-  for (int t = 0; t < BATCH; ++t) rv[t] = __ldg(Rr + (size_t)t * C4);
-  uint4 qv[QPL];
+  for (int t = 0; t < BATCH; ++t) rv[t] = __ldg(Rr + (size_t)t * (RK / 4));
+  if (cb == 0) {
+    // raw q rows into the entry (the text keys use q) and b = q . dmu
+    constexpr int QCH = G * kD * S / 16;
+    const uint4* qsrc = reinterpret_cast<const uint4*>(qu);
+    uint4* qdst = reinterpret_cast<uint4*>(ent + E::OFF_Q);
+    for (int e = lane; e < QCH; e += 32) qdst[e] = __ldg(qsrc + e);
+    const float4 dm = p.dmu ? __ldg(reinterpret_cast<const float4*>(p.dmu + (size_t)u * kD) + lane)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+    float* be = reinterpret_cast<float*>(ent + E::OFF_B);
 #pragma unroll
-  for (int t = 0; t < QPL; ++t)
-    if (lane + 32 * t < QCH) qv[t] = __ldg(qsrc + lane + 32 * t);
-  const float4 dm = p.dmu ? __ldg(reinterpret_cast<const float4*>(p.dmu + (size_t)u * kD) + lane)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-  __syncwarp();  // previous readers of this entry are done
-  uint4* qdst = reinterpret_cast<uint4*>(ent + E::OFF_Q);
-#pragma unroll
-  for (int t = 0; t < QPL; ++t)
-    if (lane + 32 * t < QCH) qdst[lane + 32 * t] = qv[t];
-  __syncwarp();
-  const T* qe = reinterpret_cast<const T*>(ent + E::OFF_Q);
-  float* be = reinterpret_cast<float*>(ent + E::OFF_B);
-  // b = q . dmu (lane owns channels 4*lane .. 4*lane+3)
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const T* qg = qe + g * kD + 4 * lane;
-    float sb = Elem<T>::to_f(qg[0]) * dm.x;
-    sb = fmaf(Elem<T>::to_f(qg[1]), dm.y, sb);
-    sb = fmaf(Elem<T>::to_f(qg[2]), dm.z, sb);
-    sb = fmaf(Elem<T>::to_f(qg[3]), dm.w, sb);
-    sb = warp_sum(sb);
-    if (lane == 0) be[g] = sb * p.sl;
+    for (int g = 0; g < G; ++g) {
+      const T* qg = qu + g * kD + 4 * lane;
+      float sb = Elem<T>::to_f(__ldg(qg)) * dm.x;
+      sb = fmaf(Elem<T>::to_f(__ldg(qg + 1)), dm.y, sb);
+      sb = fmaf(Elem<T>::to_f(__ldg(qg + 2)), dm.z, sb);
+      sb = fmaf(Elem<T>::to_f(__ldg(qg + 3)), dm.w, sb);
+      sb = warp_sum(sb);
+      if (lane == 0) be[g] = sb * p.sl;
+    }
   }
-  // q~: lane accumulates columns 4j..4j+3 over its contiguous row block; q rows are read
-  // 16 bytes at a time from the entry
   float acc[G][4];
 #pragma unroll
   for (int g = 0; g < G; ++g) acc[g][0] = acc[g][1] = acc[g][2] = acc[g][3] = 0.f;
-  const unsigned char* qrow0 = ent + E::OFF_Q + (size_t)r0 * NR * S;
 #pragma unroll
   for (int s0 = 0; s0 < NR; s0 += BATCH) {
     if (s0 > 0) {
 #pragma unroll
-      for (int t = 0; t < BATCH; ++t) rv[t] = __ldg(Rr + (size_t)(s0 + t) * C4);
+      for (int t = 0; t < BATCH; ++t) rv[t] = __ldg(Rr + (size_t)(s0 + t) * (RK / 4));
     }
 #pragma unroll
     for (int g = 0; g < G; ++g) {
+      const uint4* qrow = reinterpret_cast<const uint4*>(qu + g * kD + r0 * NR + s0);
 #pragma unroll
       for (int v = 0; v < BATCH / QV; ++v) {
+        const uint4 qc = __ldg(qrow + v);
         float qf[QV];
-        unpack16<T>(qrow0 + ((size_t)g * kD + s0 + v * QV) * S, qf);
+        unpack16<T>(reinterpret_cast<const unsigned char*>(&qc), qf);
 #pragma unroll
         for (int e = 0; e < QV; ++e) {
           const float4 r4 = rv[v * QV + e];
@@ -293,30 +295,49 @@ __device__ __forceinline__ void rotate_unit(const DecodeParams& p, int u, int la
     float* qt = reinterpret_cast<float*>(ent);
 #pragma unroll
     for (int g = 0; g < G; ++g)
-      *reinterpret_cast<float4*>(qt + g * RK + 4 * j) =
+      *reinterpret_cast<float4*>(qt + g * RK + cb * CW + 4 * j) =
           make_float4(acc[g][0] * p.sl, acc[g][1] * p.sl, acc[g][2] * p.sl, acc[g][3] * p.sl);
   }
-  __syncwarp();
 }
 
-// Pre-rotate the first NT units of the token range [a, b) into the table (kernel start).
-template <typename T, int RK, int G, int NT, int ENT>
-__device__ __forceinline__ void prerotate(const DecodeParams& p, long long a, long long b, long long L,
-                                          int lane, unsigned char* tab) {
-  const int ua = (int)(a / L), ub = (int)((b - 1) / L);
-  const int n = ub - ua + 1 < NT ? ub - ua + 1 : NT;
-  for (int k = 0; k < n; ++k) rotate_unit<T, RK, G>(p, ua + k, lane, tab + k * ENT);
+// CTA-cooperative rotation of the nu units [uA, uA + nu) the CTA's range touches: work
+// items are (unit, column block); the split PU (columns per item = RK / PU) is the largest
+// power of two with nu * PU <= warps, so the CTA's warps get ~one item each.
+template <typename T, int RK, int G, int PU, int ENT>
+__device__ __forceinline__ void rotate_items(const DecodeParams& p, int uA, int nu, int w, int nw,
+                                             int lane, unsigned char* tab) {
+  for (int it = w; it < nu * PU; it += nw)
+    rotate_cols<T, RK, RK / PU, G>(p, uA + it / PU, it % PU, lane, tab + (it / PU) * ENT);
 }
 
-// Table entry of unit u for a warp whose range starts in unit ua (rotates lazily when the
-// range touches more than NT units; the slot's previous unit is finished by then).
-template <typename T, int RK, int G, int NT, int ENT>
-__device__ __forceinline__ unsigned char* unit_entry(const DecodeParams& p, int u, int ua, int lane,
-                                                     unsigned char* tab) {
-  const int k = u - ua;
-  unsigned char* ent = tab + (k % NT) * ENT;
-  if (k >= NT) rotate_unit<T, RK, G>(p, u, lane, ent);
-  return ent;
+// Runs before any tile load is issued: issuing the first tiles before (or right after) the
+// rotation's reads was measured 1-2 us slower -- the reads queue behind the tile burst.
+template <typename T, int RK, int G, int WARPS, int ENT>
+__device__ __forceinline__ void rotate_cta(const DecodeParams& p, int uA, int nu, int w, int lane,
+                                           unsigned char* tab) {
+  constexpr int S = sizeof(T);
+  int pu = 1;
+  while (2 * pu * nu <= WARPS && 2 * pu <= 8) pu *= 2;
+  // columns per item must keep >= one 16-byte q chunk of rows per lane: CW >= 4 * (16/S) / (kD/32)
+  constexpr int CWMIN = (16 / S) * 4 * 32 / kD;
+  if (pu >= 8 && RK / 8 >= CWMIN)
+    rotate_items<T, RK, G, (RK / 8 >= CWMIN ? 8 : 1), ENT>(p, uA, nu, w, WARPS, lane, tab);
+  else if (pu >= 4 && RK / 4 >= CWMIN)
+    rotate_items<T, RK, G, (RK / 4 >= CWMIN ? 4 : 1), ENT>(p, uA, nu, w, WARPS, lane, tab);
+  else if (pu >= 2 && RK / 2 >= CWMIN)
+    rotate_items<T, RK, G, (RK / 2 >= CWMIN ? 2 : 1), ENT>(p, uA, nu, w, WARPS, lane, tab);
+  else
+    rotate_items<T, RK, G, 1, ENT>(p, uA, nu, w, WARPS, lane, tab);
+  __syncthreads();
+}
+
+// the CTA's token range [ca, cb) (union of its warps' ranges) and the units it touches
+__device__ __forceinline__ void cta_units(long long Ttot, int NW, int WARPS, int blk, long long L,
+                                          int& uA, int& nu) {
+  const int w0 = blk * WARPS, w1 = (blk + 1) * WARPS < NW ? (blk + 1) * WARPS : NW;
+  const long long ca = range_start(Ttot, w0, NW), cb = range_start(Ttot, w1, NW);
+  uA = (int)(ca / L);
+  nu = cb > ca ? (int)((cb - 1) / L) - uA + 1 : 0;
 }
 
 // One tile: scores (key rows of KR channels), online-softmax rescale, P.V.
@@ -433,19 +454,21 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   constexpr int NACC = C::NACC;
   extern __shared__ __align__(128) unsigned char fsm[];
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = (int)((blockIdx.x + p.rot) % gridDim.x) * WARPS + w;
-  if (gw >= NW) return;
+  const int gw = blockIdx.x * p.aw + w;
   unsigned char* base = fsm + w * C::WARP_SMEM;
   float* qs = reinterpret_cast<float*>(base + C::OFF_Q);
   float* pbuf = reinterpret_cast<float*>(base + C::OFF_P);
-  unsigned char* tab = base + C::OFF_TAB;
+  unsigned char* tab = fsm + C::OFF_TAB;
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
 
   const int N = p.N, M = p.M;
   const long long L = (long long)N + M;
   const long long Ttot = L * p.U;
+  RK_TRACE(0, gtime());
+  int uA, nu;
+  cta_units(Ttot, NW, p.aw, blockIdx.x, L, uA, nu);
   const long long a = range_start(Ttot, gw, NW), b = range_start(Ttot, gw + 1, NW);
-  if (a >= b) return;
+  const bool active = w < p.aw && gw < NW && a < b;
 
   const T* Kc = static_cast<const T*>(p.Kc);
   const T* V = static_cast<const T*>(p.V);
@@ -453,15 +476,11 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   const T* Vt = static_cast<const T*>(p.Vt);
   const uint64_t pol = policy_evict_first();
 
-  if (lane == 0) {
+  if (active && lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
   __syncwarp();
-  RK_TRACE(0, gtime());
-  const int ua = (int)(a / L);
-  prerotate<T, RK, G, C::NT, C::ENT>(p, a, b, L, lane, tab);
-  RK_TRACE(1, gtime());
 
   // ---------------- producer (lane 0): issue the tile at cursor px into stage st
   long long px = a;
@@ -481,6 +500,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
     }
     px += tl.tn;
   };
+  rotate_cta<T, RK, G, WARPS, C::ENT>(p, uA, nu, w, lane, tab);  // query table, then tiles
+  RK_TRACE(1, gtime());
+  if (!active) return;
   if (lane == 0)
     for (int s = 0; s < STAGES && px < b; ++s) issue(s);
 
@@ -492,7 +514,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   const float* qts = nullptr;  // current unit's scaled q~ [G][RK] and bias [G] (table entry)
   const float* bs = nullptr;
   auto setup = [&](int u) {
-    const unsigned char* ent = unit_entry<T, RK, G, C::NT, C::ENT>(p, u, ua, lane, tab);
+    const unsigned char* ent = tab + (u - uA) * C::ENT;
     using E = QEnt<T, RK, G>;
     qts = reinterpret_cast<const float*>(ent);
     bs = reinterpret_cast<const float*>(ent + E::OFF_B);
@@ -612,8 +634,9 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   RK_TRACE(3, gtime());
   if (cur_u >= 0) flush(cur_u);
   RK_TRACE(4, gtime());
+
   RK_TRACE(5, (unsigned long long)j);
-  RK_TRACE(6, (unsigned long long)(cur_u - ua + 1));
+  RK_TRACE(6, (unsigned long long)nu);
   if (p.trace != nullptr && lane == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));

@@ -64,12 +64,12 @@ struct GqaCfg {
   static constexpr int TX = (STAGE / 512) / 16 * 16;  // text tile tokens (4 halves fit a stage)
   static constexpr int XH = TX * 128;               // one 64-channel text half
   static constexpr int NSTG = STAGES;
-  static constexpr int NT = 2;                                 // pre-rotated units
-  static constexpr int ENT = QEnt<__nv_bfloat16, RK, G>::BYTES;
-  static constexpr int OFF_TAB = NSTG * STAGE;                 // QEnt [NT]
-  static constexpr int OFF_BAR = OFF_TAB + NT * ENT;
+  static constexpr int OFF_BAR = NSTG * STAGE;
   static constexpr int WARP_SMEM = (OFF_BAR + 8 * NSTG + 1023) / 1024 * 1024;
-  static constexpr int SMEM = WARPS * WARP_SMEM + 1024;        // + alignment slack
+  static constexpr int CAP = 8;                                // CTA query table (units)
+  static constexpr int ENT = QEnt<__nv_bfloat16, RK, G>::BYTES;
+  static constexpr int OFF_TAB = WARPS * WARP_SMEM;
+  static constexpr int SMEM = OFF_TAB + CAP * ENT + 1024;      // + alignment slack
   static_assert(STAGE >= 4 * XH && TX >= 16, "text tile must fit the stage");
   static_assert(TT % 16 == 0 && KB % 1024 == 0, "tile");
   static_assert(RK == 32 || RK == 64, "rank");
@@ -88,24 +88,22 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   extern __shared__ unsigned char gsm_raw[];
   unsigned char* gsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = (int)((blockIdx.x + p.rot) % gridDim.x) * WARPS + w;
-  if (gw >= NW) return;
+  const int gw = blockIdx.x * p.aw + w;
   unsigned char* base = gsm + w * C::WARP_SMEM;
-  unsigned char* tab = base + C::OFF_TAB;
+  unsigned char* tab = gsm + C::OFF_TAB;
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
   const uint32_t sbase = smem_u32(base);
 
   const int N = p.N, M = p.M;
   const long long L = (long long)N + M;
   const long long Ttot = L * p.U;
-  const long long a = range_start(Ttot, gw, NW), b = range_start(Ttot, gw + 1, NW);
-  if (a >= b) return;
   RK_TRACE(0, gtime());
-  const int ua = (int)(a / L);
-  prerotate<__nv_bfloat16, RK, G, C::NT, C::ENT>(p, a, b, L, lane, tab);  // before any tile load
-  RK_TRACE(1, gtime());
+  int uA, nu;
+  cta_units(Ttot, NW, p.aw, blockIdx.x, L, uA, nu);
+  const long long a = range_start(Ttot, gw, NW), b = range_start(Ttot, gw + 1, NW);
+  const bool active = w < p.aw && gw < NW && a < b;
   const uint64_t pol = policy_evict_first();
-  if (lane == 0) {
+  if (active && lane == 0) {
     for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
     tc::prefetch_tmap(&maps.kc);
@@ -136,6 +134,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     }
     px += tl.tn;
   };
+  rotate_cta<__nv_bfloat16, RK, G, WARPS, C::ENT>(p, uA, nu, w, lane, tab);  // query table, then tiles
+  RK_TRACE(1, gtime());
+  if (!active) return;
   if (lane == 0)
     for (int s = 0; s < STAGES && px < b; ++s) issue(s);
 
@@ -151,7 +152,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   auto setup = [&](int u) {
     // q~ = q R_r, b = q . dmu and q of the unit's G heads from the warp's rotation table
     using E = QEnt<__nv_bfloat16, RK, G>;
-    const unsigned char* ent = unit_entry<__nv_bfloat16, RK, G, C::NT, C::ENT>(p, u, ua, lane, tab);
+    const unsigned char* ent = tab + (u - uA) * C::ENT;
     const float* qts = reinterpret_cast<const float*>(ent);
     const float* bs = reinterpret_cast<const float*>(ent + E::OFF_B);
     // A fragments straight from global memory (all loads independent): row g holds the
@@ -343,8 +344,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   RK_TRACE(3, gtime());
   if (cur_u >= 0) flush(cur_u);
   RK_TRACE(4, gtime());
+
   RK_TRACE(5, (unsigned long long)j);
-  RK_TRACE(6, (unsigned long long)(cur_u - ua + 1));
+  RK_TRACE(6, (unsigned long long)nu);
   if (p.trace != nullptr && lane == 0) {
     unsigned smid;
     asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));

@@ -90,8 +90,8 @@ def trace_shape(U, G, N, M, r, d=128, kernel=0):
     rel = (t[:, :5] - t0).double() / 1e3
     q = torch.tensor([0.0, 0.5, 0.9, 1.0], dtype=torch.double)
     names = ["start", "rotated", "tile0", "loopend", "end"]
-    print(f"trace U={U} G={G} N={N} M={M} r={r}: warps={t.shape[0]} tiles/warp "
-          f"{t[:, 5].double().mean():.1f} units/warp max {int(t[:, 6].max())}")
+    print(f"trace U={U} G={G} N={N} M={M} r={r} kernel={kernel}: warps={t.shape[0]} "
+          f"tiles/warp {t[:, 5].double().mean():.1f} units/CTA max {int(t[:, 6].max())}")
     for k, nm in enumerate(names):
         v = torch.quantile(rel[:, k], q).tolist()
         print(f"   {nm:8s} min {v[0]:7.2f}  med {v[1]:7.2f}  p90 {v[2]:7.2f}  max {v[3]:7.2f} us")
@@ -164,7 +164,8 @@ def main():
         return
     if sys.argv[1:2] == ["--trace"]:
         for sh in sys.argv[2:]:
-            trace_shape(*(int(x) for x in sh.split(",")))
+            trace_shape(*(int(x) for x in sh.split(",")[:5]),
+                        kernel=int(sh.split(",")[5]) if sh.count(",") >= 5 else 0)
         return
     shapes = sys.argv[1:] or [
         "128,7,4096,128,32", "128,7,1024,128,32", "128,7,2048,128,32", "128,7,8192,128,32",
