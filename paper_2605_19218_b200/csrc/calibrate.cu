@@ -4,6 +4,7 @@
 //   P:653) -> top-r select + compaction + delta_mu.
 #include <cfloat>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "internal.h"
@@ -378,7 +379,7 @@ __global__ void __launch_bounds__(kJacobiThreads) jacobi_kernel(int d, const dou
 // ------------------------------------------------------------------------------------------
 // fp32 Jacobi, full storage (row stride d+1: row and column passes are both bank-conflict
 // free), 1024 threads per CTA (one CTA per SM; 32 warps hide the shared-memory latency of the
-// rotation passes).  A round: (1) d/2 threads compute the Schur rotations of the round's
+// rotation passes).  Generic-d fallback; d = 128 runs jacobi32p_kernel below.  A round: (1) d/2 threads compute the Schur rotations of the round's
 // disjoint pairs, (2) row pass A <- J^T A over all (pair, column), (3) column pass A <- A J
 // and V <- V J over all (row, pair).  Followed by refine_kernel (fp64).
 constexpr int kJ32Threads = 1024;
@@ -504,6 +505,178 @@ __global__ void __launch_bounds__(kJ32Threads, 1) jacobi32_kernel(int d_rt, cons
     }
   }
   for (int j = tid; j < d; j += nth) lam_out[(size_t)u * d + j] = (float)((double)A[j * ld + j] * unscale);
+  for (int e = tid; e < d * d; e += nth) vecs[(size_t)u * d * d + e] = V[(e / d) * ld + (e % d)];
+  if (tid == 0) jinfo[u] = converged ? 0 : (sweep > 0 ? sweep : 1);
+}
+
+// ------------------------------------------------------------------------------------------
+// fp32 Jacobi, packed symmetric A, TWO CTAs per SM (default for d = 128).  A is kept as its
+// upper triangle (33 KB) so that two matrices share an SM: one CTA's rotation-parameter
+// phase and barriers (latency-bound, ~40% of the issue slots of the one-CTA kernel, ncu)
+// overlap the other's update passes.  A round is one fused pass: each of the h(h+1)/2
+// upper 2x2 blocks (pair a <= pair b) becomes J_a^T X J_b (every element of A read and
+// written once), and V <- V J, between two barriers.
+constexpr int kJPThreads = 512;
+
+size_t jacobi32p_smem_bytes(int d) {
+  const int h = d / 2;
+  const size_t np = (size_t)d * (d + 1) / 2, nblk = (size_t)h * (h + 1) / 2;
+  size_t b = (np + (size_t)d * (d + 1)) * 4;      // A packed, V [d][d+1]
+  b += (size_t)h * 8 + h * 4 + 32 * 4 + h * 4;    // csn, tt, red, PQ
+  b += (size_t)d * 4 + nblk * 4;                  // rowoff, blk
+  return (b + 15) & ~(size_t)15;
+}
+
+template <int DC>
+__global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* __restrict__ cq,
+                                                                  float* __restrict__ lam_out,
+                                                                  float* __restrict__ vecs,
+                                                                  int32_t* __restrict__ jinfo, float tol,
+                                                                  int max_sweeps) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int d = DC, h = DC / 2, ld = DC + 1;
+  constexpr int np = d * (d + 1) / 2, nblk = h * (h + 1) / 2;
+  constexpr int nth = kJPThreads;
+  const int u = blockIdx.x, tid = threadIdx.x;
+  float* A = reinterpret_cast<float*>(smem_raw);                 // packed upper triangle
+  float* V = A + np;                                              // [d][ld]
+  float2* csn = reinterpret_cast<float2*>(V + d * ld);            // (np + d*ld) even: 8-B aligned
+  float* tt = reinterpret_cast<float*>(csn + h);
+  float* red = tt + h;
+  uint32_t* PQ = reinterpret_cast<uint32_t*>(red + 32);
+  int* rowoff = reinterpret_cast<int*>(PQ + h);                   // packed index of (i, 0) shifted
+  uint32_t* blk = reinterpret_cast<uint32_t*>(rowoff + d);        // (a | b << 16), a <= b
+  __shared__ double s_red[32];
+  __shared__ int s_bad;
+  // packed index of (i, j), i <= j:  rowoff[i] + j  with rowoff[i] = i*d - i*(i-1)/2 - i
+  auto pk = [&](int i, int j) { return i <= j ? rowoff[i] + j : rowoff[j] + i; };
+
+  const double* C = cq + (size_t)u * d * d;
+  double f2 = 0.0;
+  int bad = 0;
+  for (int e = tid; e < d * d; e += nth) {
+    const double x = C[e];
+    if (!isfinite(x)) bad = 1;
+    f2 = fma(x, x, f2);
+  }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  if (bad) s_bad = 1;
+  f2 = block_sum<double>(f2, s_red);
+  __syncthreads();
+  if (s_bad) {
+    for (int e = tid; e < d * d; e += nth) vecs[(size_t)u * d * d + e] = 0.f;
+    for (int j = tid; j < d; j += nth) lam_out[(size_t)u * d + j] = CUDART_NAN_F;
+    if (tid == 0) jinfo[u] = -1;
+    return;
+  }
+  int ex = 0;
+  if (f2 > 0.0) frexp(sqrt(f2), &ex);
+  const double scale = ldexp(1.0, -ex), unscale = ldexp(1.0, ex);
+  for (int i = tid; i < d; i += nth) rowoff[i] = i * d - (i * (i - 1)) / 2 - i;
+  for (int e = tid; e < nblk; e += nth) {
+    int a = 0, rem = e;
+    while (rem >= h - a) { rem -= h - a; ++a; }
+    blk[e] = (uint32_t)a | ((uint32_t)(a + rem) << 16);
+  }
+  for (int e = tid; e < d * ld; e += nth) V[e] = (e / ld == e % ld) ? 1.f : 0.f;
+  __syncthreads();
+  for (int e = tid; e < d * d; e += nth) {
+    const int i = e / d, j = e % d;
+    if (i <= j) A[rowoff[i] + j] = (float)(C[e] * scale);
+  }
+  __syncthreads();
+  // squared Frobenius norms summed element by element (a difference of packed and diagonal
+  // sums would cancel catastrophically in fp32 near convergence)
+  float fro2 = 0.f;
+  for (int e = tid; e < d * d; e += nth) {
+    const int i = e / d, j = e % d;
+    if (i <= j) { const float a = A[rowoff[i] + j]; fro2 = fmaf(i == j ? a : 2.f * a, a, fro2); }
+  }
+  fro2 = block_sum<float>(fro2, red);
+
+  int sweep = 0, converged = 0;
+  for (;; ++sweep) {
+    float off2 = 0.f;
+    for (int e = tid; e < d * d; e += nth) {
+      const int i = e / d, j = e % d;
+      if (i < j) { const float a = A[rowoff[i] + j]; off2 = fmaf(2.f * a, a, off2); }
+    }
+    off2 = block_sum<float>(off2, red);
+    if (off2 <= tol * tol * fro2) { converged = 1; break; }
+    if (sweep >= max_sweeps) break;
+    for (int k = 0; k < d - 1; ++k) {
+      if (tid < h) {
+        // circle-method pairs (no p < q swap: the rotation is symmetric in p and q)
+        int p, q;
+        if (tid == 0) { p = k; q = d - 1; }
+        else {
+          p = k + tid; if (p >= d - 1) p -= d - 1;
+          q = k - tid; if (q < 0) q += d - 1;
+        }
+        const float apq = A[pk(p, q)];
+        float c = 1.f, s = 0.f, t = 0.f;
+        if (apq != 0.f) {
+          const float app = A[rowoff[p] + p], aqq = A[rowoff[q] + q];
+          const float tau = (aqq - app) / (2.f * apq);
+          t = (tau >= 0.f ? 1.f : -1.f) / (fabsf(tau) + sqrtf(1.f + tau * tau));
+          c = 1.f / sqrtf(1.f + t * t);  // correctly rounded (see jacobi32_kernel)
+          s = t * c;
+        }
+        csn[tid] = make_float2(c, s);
+        tt[tid] = t;
+        PQ[tid] = (uint32_t)p | ((uint32_t)q << 16);
+      }
+      __syncthreads();
+      // A <- J^T A J over the upper blocks (pair a <= pair b)
+      for (int e = tid; e < nblk; e += nth) {
+        const uint32_t ab = blk[e];
+        const int a = ab & 0xFFFF, b = ab >> 16;
+        const uint32_t pqa = PQ[a];
+        const int pa = pqa & 0xFFFF, qa = pqa >> 16;
+        if (a == b) {
+          const int ipq = pk(pa, qa);
+          const float apq = A[ipq], t = tt[a];
+          A[rowoff[pa] + pa] -= t * apq;
+          A[rowoff[qa] + qa] += t * apq;
+          A[ipq] = 0.f;
+        } else {
+          const uint32_t pqb = PQ[b];
+          const int pb = pqb & 0xFFFF, qb = pqb >> 16;
+          const float2 ca2 = csn[a], cb2 = csn[b];
+          const float ca = ca2.x, sa = ca2.y, cb = cb2.x, sb = cb2.y;
+          const int i00 = pk(pa, pb), i01 = pk(pa, qb), i10 = pk(qa, pb), i11 = pk(qa, qb);
+          const float x00 = A[i00], x01 = A[i01], x10 = A[i10], x11 = A[i11];
+          const float l00 = ca * x00 - sa * x10, l01 = ca * x01 - sa * x11;
+          const float l10 = sa * x00 + ca * x10, l11 = sa * x01 + ca * x11;
+          A[i00] = cb * l00 - sb * l01;
+          A[i01] = sb * l00 + cb * l01;
+          A[i10] = cb * l10 - sb * l11;
+          A[i11] = sb * l10 + cb * l11;
+        }
+      }
+      // V <- V J: warp w owns pairs w + 16 i, lanes own rows (conflict-free)
+      {
+        const int lane = tid & 31, wv = tid >> 5;
+#pragma unroll
+        for (int i = 0; i < h / (nth / 32); ++i) {
+          const int b = wv + i * (nth / 32);
+          const uint32_t pqb = PQ[b];
+          const int pb = pqb & 0xFFFF, qb = pqb >> 16;
+          const float2 c2 = csn[b];
+#pragma unroll
+          for (int jx = 0; jx < d / 32; ++jx) {
+            const int x = lane + 32 * jx;
+            const float vx = V[x * ld + pb], vy = V[x * ld + qb];
+            V[x * ld + pb] = c2.x * vx - c2.y * vy;
+            V[x * ld + qb] = c2.y * vx + c2.x * vy;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (int j = tid; j < d; j += nth) lam_out[(size_t)u * d + j] = (float)((double)A[rowoff[j] + j] * unscale);
   for (int e = tid; e < d * d; e += nth) vecs[(size_t)u * d * d + e] = V[(e / d) * ld + (e % d)];
   if (tid == 0) jinfo[u] = converged ? 0 : (sweep > 0 ? sweep : 1);
 }
@@ -645,8 +818,9 @@ int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st) {
   float* v32 = ws.v32;
   size_t sm = jacobi32_smem_bytes(d);
   if (d == 128) {
-    cudaFuncSetAttribute(jacobi32_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    jacobi32_kernel<128><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
+    const size_t smp = jacobi32p_smem_bytes(d);
+    cudaFuncSetAttribute(jacobi32p_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+    jacobi32p_kernel<128><<<U, kJPThreads, smp, st>>>(ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
   } else {
     cudaFuncSetAttribute(jacobi32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     jacobi32_kernel<0><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
