@@ -206,6 +206,35 @@ rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dims, const void* q,
                                       rotatek_stream_t stream);
 
 /*
+ * Token-sharded decode (when there are fewer units than GPUs, the token axis
+ * is split across ranks).  The online-softmax split of Alg. 2 (App. C "standard online-
+ * softmax merge") is exact, so each rank runs Alg. 2 over ITS token slice -- its own
+ * [U, N_p, r] / [U, N_p, d] cache shard (N_p >= 1) and [U, M_p, d] text shard, with the
+ * replicated q, R_r and dmu -- and returns the un-normalised state instead of out:
+ *   part [U, G, d+2] fp32 device:  acc[d] | m | l   per (unit, query head), where with
+ *   z_n = s_n * log2(e) the base-2 logit of token n (s_n the 1/sqrt(d)-scaled score of
+ *   Alg. 2 l.3-4):  m = max_n z_n,  l = sum_n 2^(z_n - m),  acc = sum_n 2^(z_n - m) V[n].
+ * Same arguments, workspace, layouts and errors as rotatek_decode_attn (out -> part).
+ */
+rotatek_status rotatek_decode_attn_partial(const rotatek_dims* dims, const void* q,
+                                           const void* K_comp, const void* V, const float* R,
+                                           const float* dmu, const void* K_text,
+                                           const void* V_text, float softmax_scale, float* part,
+                                           void* workspace, size_t workspace_bytes,
+                                           rotatek_stream_t stream);
+
+/*
+ * Merge P token-shard states (e.g. gathered with an all-gather) into the attention output:
+ *   parts [P, U, G, d+2] fp32 device (shard-major, rotatek_decode_attn_partial layout)
+ *   out   [U, G, d] fp32 device:  out = sum_p 2^(m_p - M) acc_p / sum_p 2^(m_p - M) l_p,
+ *         M = max_p m_p  (shards combined in index order: deterministic).
+ * Errors: DIMS, NULL, ALIGN, CUDA.
+ */
+rotatek_status rotatek_merge_partials(int32_t units, int32_t group, int32_t head_dim,
+                                      int32_t nparts, const float* parts, float* out,
+                                      rotatek_stream_t stream);
+
+/*
  * The top-r select + compaction step on its own (the selection half of
  * rotatek_calibrate, exposed so that it can be checked bit-exactly on given
  * eigenvalue arrays, including adversarial ties):

@@ -239,6 +239,35 @@ def decode(q, Kt, V, R, dmu, Ktext=None, Vtext=None, scale=0.0) -> np.ndarray:
     return out
 
 
+def decode_partial(q, Kt, V, R, dmu, Ktext=None, Vtext=None, scale=0.0) -> np.ndarray:
+    """Alg. 2 over ONE token shard, stopped before the normalisation: the online-softmax
+    state of App. C per unit and query head, written out from its definition:
+        z_n = s_n log2(e)  (s_n the scaled scores of Alg. 2 l.3-4, visual then text),
+        m = max_n z_n,  l = sum_n 2^(z_n - m),  acc = sum_n 2^(z_n - m) V_n.
+    Returns [U, G, d + 2] = acc | m | l (the layout of rotatek_decode_attn_partial)."""
+    s = scores(q, Kt, R, dmu, Ktext, scale) * np.log2(np.e)       # [U, G, N + M]
+    Vall = _f64(V) if Vtext is None else np.concatenate([_f64(V), _f64(Vtext)], axis=1)
+    m = s.max(axis=2)
+    w = np.exp2(s - m[:, :, None])
+    U, G, _ = s.shape
+    out = np.empty((U, G, Vall.shape[2] + 2))
+    out[:, :, :-2] = np.einsum("ugn,und->ugd", w, Vall)
+    out[:, :, -2] = m
+    out[:, :, -1] = w.sum(axis=2)
+    return out
+
+
+def merge_partials(parts) -> np.ndarray:
+    """Merge token-shard states [P, U, G, d+2]: M = max_p m_p,
+    out = sum_p 2^(m_p - M) acc_p / sum_p 2^(m_p - M) l_p."""
+    parts = _f64(parts)
+    m = parts[..., -2]
+    M = m.max(axis=0)
+    f = np.exp2(m - M[None])
+    acc = (parts[..., :-2] * f[..., None]).sum(axis=0)
+    return acc / (parts[..., -1] * f).sum(axis=0)[..., None]
+
+
 def scores(q, Kt, R, dmu, Ktext=None, scale=0.0) -> np.ndarray:
     """Alg. 2 lines 1-5: concatenated scores [U, G, N + M] (visual first)."""
     q = _f64(q)

@@ -225,6 +225,55 @@ rotatek_status rotatek_decode_attn(const rotatek_dims* dm, const void* q, const 
                                 workspace, workspace_bytes, 0, 0, stream);
 }
 
+rotatek_status rotatek_decode_attn_partial(const rotatek_dims* dm, const void* q, const void* K_comp,
+                                           const void* V, const float* R, const float* dmu,
+                                           const void* K_text, const void* V_text, float softmax_scale,
+                                           float* part, void* workspace, size_t workspace_bytes,
+                                           rotatek_stream_t stream) {
+  g_launches = 0;
+  rotatek_status s = check_dims(dm);
+  if (s != ROTATEK_OK) return s;
+  const int M = dm->n_text;
+  if (!q || !K_comp || !V || !R || !part) return fail(ROTATEK_ERR_NULL, "q, K_comp, V, R, part are required");
+  if (M > 0 && (!K_text || !V_text)) return fail(ROTATEK_ERR_NULL, "K_text/V_text required when n_text > 0");
+  const void* ptrs[] = {q, K_comp, V, R, dmu, K_text, V_text, workspace};
+  for (const void* p : ptrs)
+    if (p && !aligned16(p)) return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
+  if (reinterpret_cast<uintptr_t>(part) & 3u) return fail(ROTATEK_ERR_ALIGN, "part not 4-byte aligned");
+  rk::DecodeWs ws;
+  const size_t need = rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->rank, dm->n_vis, M,
+                                           workspace, &ws);
+  if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
+  rk::DecodeArgs a;
+  a.U = dm->units; a.G = dm->group; a.d = dm->head_dim; a.r = dm->rank; a.N = dm->n_vis; a.M = M;
+  a.bf16 = dm->dtype == ROTATEK_BF16;
+  a.q = q; a.Kc = K_comp; a.V = V; a.R = R; a.dmu = dmu;
+  a.Kt = M > 0 ? K_text : nullptr; a.Vt = M > 0 ? V_text : nullptr;
+  a.scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf((float)dm->head_dim);
+  a.out = nullptr;
+  a.pout = part;
+  int n = 0;
+  if ((s = launched(rk::launch_decode(a, ws, 0, 0, reinterpret_cast<cudaStream_t>(stream)), &n))) return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
+rotatek_status rotatek_merge_partials(int32_t units, int32_t group, int32_t head_dim, int32_t nparts,
+                                      const float* parts, float* out, rotatek_stream_t stream) {
+  g_launches = 0;
+  if (units < 1 || group < 1 || head_dim < 1 || head_dim > 256 || nparts < 1)
+    return fail(ROTATEK_ERR_DIMS, "bad merge dims");
+  if (!parts || !out) return fail(ROTATEK_ERR_NULL, "parts and out are required");
+  if ((reinterpret_cast<uintptr_t>(parts) & 3u) || !aligned16(out))
+    return fail(ROTATEK_ERR_ALIGN, "parts 4-byte / out 16-byte alignment");
+  int n = 0;
+  rotatek_status s = launched(rk::launch_merge_parts(units, group, head_dim, nparts, parts, out,
+                                                     reinterpret_cast<cudaStream_t>(stream)), &n);
+  if (s) return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
 rotatek_status rotatek_select_topr(int32_t units, int32_t head_dim, int32_t rank,
                                    const float* eigvals, uint32_t* keep_mask, int32_t* keep_idx,
                                    int32_t* info, rotatek_stream_t stream) {

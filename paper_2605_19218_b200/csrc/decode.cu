@@ -49,6 +49,7 @@ struct DecodeParams {
   float* partials;
   unsigned long long* trace = nullptr;  // diagnostics: [NW][8] globaltimer stamps (or null)
   int aw = 0;                           // active (streaming) warps per CTA (<= WARPS)
+  float* pout = nullptr;                // partial-state output [U][G][d+2] (token shards) or null
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -173,7 +174,13 @@ __global__ void __launch_bounds__(kGenWarps * 32) decode_generic_kernel(DecodePa
       A = fmaf(wacc[(size_t)(ww * G + g) * d + c], f, A);
     }
     if (splits == 1) {
-      p.out[((size_t)u * G + g) * d + c] = A / L;
+      if (p.pout) {
+        float* po = p.pout + ((size_t)u * G + g) * (d + 2);
+        po[c] = A;
+        if (c == 0) { po[d] = M; po[d + 1] = L; }
+      } else {
+        p.out[((size_t)u * G + g) * d + c] = A / L;
+      }
     } else {
       float* dst = part + (((size_t)u * G + g) * splits + split) * (d + 2);
       if (c == 0) { dst[0] = M; dst[1] = L; }
@@ -199,7 +206,13 @@ __global__ void __launch_bounds__(kGenWarps * 32) decode_generic_kernel(DecodePa
       L = fmaf(__ldcg(src + (size_t)s * (d + 2) + 1), f, L);
       A = fmaf(__ldcg(src + (size_t)s * (d + 2) + 2 + c), f, A);
     }
-    p.out[((size_t)u * G + g) * d + c] = A / L;
+    if (p.pout) {
+      float* po = p.pout + ((size_t)u * G + g) * (d + 2);
+      po[c] = A;
+      if (c == 0) { po[d] = M; po[d + 1] = L; }
+    } else {
+      p.out[((size_t)u * G + g) * d + c] = A / L;
+    }
   }
   if (tid == 0) p.counters[u] = 0u;
 }
@@ -298,7 +311,7 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
   const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw};
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout};
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)) return -1;
   return 1;
 }
@@ -411,7 +424,7 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
   if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
   const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw};
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout};
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, pl.cmax)) return -1;
   return 1;
 }
@@ -471,7 +484,7 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
   int S = splits > 0 ? splits : decode_max_splits(a.U, a.N, a.M);
   if (S > ws.max_splits) S = ws.max_splits;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials};
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, nullptr, 0, a.pout};
   size_t sm = ((size_t)a.G * a.d + (size_t)a.G * a.r + a.G + 2 * kGenWarps * a.G +
                (size_t)kGenWarps * a.G * a.d) * sizeof(float);
   dim3 grid(S, a.U);
@@ -482,6 +495,39 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
     cudaFuncSetAttribute(decode_generic_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     decode_generic_kernel<float><<<grid, kGenWarps * 32, sm, st>>>(p, S);
   }
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// =====================================================================================
+// merge of token-shard partial states (token-sharded decode for U < P):
+//   out[u][g] = sum_p 2^(m_p - M) acc_p / sum_p 2^(m_p - M) l_p,   M = max_p m_p
+// parts [P][U][G][d+2] (acc[d] | m | l, m in base-2 logit units), shards merged in order.
+// =====================================================================================
+__global__ void __launch_bounds__(128) merge_parts_kernel(int P, int UG, int d, const float* __restrict__ parts,
+                                                          float* __restrict__ out) {
+  const int ug = blockIdx.x;
+  const size_t rec = (size_t)(d + 2), stride = (size_t)UG * rec;
+  const float* base = parts + (size_t)ug * rec;
+  float M = -CUDART_INF_F;
+  for (int s = 0; s < P; ++s) M = fmaxf(M, base[s * stride + d]);
+  float L = 0.f;
+  for (int s = 0; s < P; ++s) {
+    const float ms = base[s * stride + d];
+    L = fmaf(base[s * stride + d + 1], ms == -CUDART_INF_F ? 0.f : fast_exp2(ms - M), L);
+  }
+  const float inv = 1.f / L;
+  for (int c = threadIdx.x; c < d; c += blockDim.x) {
+    float A = 0.f;
+    for (int s = 0; s < P; ++s) {
+      const float ms = base[s * stride + d];
+      A = fmaf(base[s * stride + c], ms == -CUDART_INF_F ? 0.f : fast_exp2(ms - M), A);
+    }
+    out[(size_t)ug * d + c] = A * inv;
+  }
+}
+
+int launch_merge_parts(int U, int G, int d, int P, const float* parts, float* out, cudaStream_t st) {
+  merge_parts_kernel<<<U * G, 128, 0, st>>>(P, U * G, d, parts, out);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -134,9 +134,12 @@ __device__ __forceinline__ void load_v4<float>(const unsigned char* p, float* f)
 // order = range order, so the result is deterministic) and write out[g][:] = acc / l.
 // All G heads and two slots are in flight at once: the merge is latency-bound on L2 reads
 // and sits on the kernel's tail.
+// pout != null (token-shard partial mode): write the merged state acc | m | l per head to
+// pout [G][kD + 2] instead of the normalised output.
 template <int G>
 __device__ __forceinline__ void merge_unit(const float* __restrict__ part, int count,
-                                           float* __restrict__ out, int lane) {
+                                           float* __restrict__ out, int lane,
+                                           float* __restrict__ pout = nullptr) {
   constexpr int kRec = kD + 4;
   // pass 1 (lanes over slots): per-head max of m and the merged denominator
   // sum_s l_s 2^(m_s - max)
@@ -178,6 +181,16 @@ __device__ __forceinline__ void merge_unit(const float* __restrict__ part, int c
       A[g][0] = fmaf(v.x, f, A[g][0]); A[g][1] = fmaf(v.y, f, A[g][1]);
       A[g][2] = fmaf(v.z, f, A[g][2]); A[g][3] = fmaf(v.w, f, A[g][3]);
     }
+  }
+  if (pout) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float* po = pout + (size_t)g * (kD + 2);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) po[lane * 4 + k] = A[g][k];
+      if (lane == 0) { po[kD] = mloc[g]; po[kD + 1] = Ls[g]; }
+    }
+    return;
   }
 #pragma unroll
   for (int g = 0; g < G; ++g) {
@@ -551,7 +564,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
     if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], 1u);
     prev = __shfl_sync(0xffffffffu, prev, 0);
     if (prev != (unsigned)(count - 1)) return;
-    merge_unit<G>(p.partials + ((size_t)u * cmax) * G * kRec, count, p.out + (size_t)u * G * kD, lane);
+    merge_unit<G>(p.partials + ((size_t)u * cmax) * G * kRec, count, p.out + (size_t)u * G * kD, lane,
+                  p.pout ? p.pout + (size_t)u * G * (kD + 2) : nullptr);
     if (lane == 0) p.counters[u] = 0u;
   };
   auto flush = [&](int u) {
@@ -568,6 +582,16 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
 #pragma unroll
         for (int aa = 1; aa < NACC; ++aa) A[g][k] += acc[aa][g][k];
       }
+    }
+    if (count == 1 && p.pout) {
+#pragma unroll
+      for (int g = 0; g < G; ++g) {
+        float* po = p.pout + ((size_t)u * G + g) * (kD + 2);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) po[lane * 4 + k] = A[g][k];
+        if (lane == 0) { po[kD] = m[g]; po[kD + 1] = lt[g]; }
+      }
+      return;
     }
     if (count == 1) {
 #pragma unroll

@@ -245,7 +245,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], 1u);
     prev = __shfl_sync(0xffffffffu, prev, 0);
     if (prev != (unsigned)(count - 1)) return;
-    merge_unit<G>(p.partials + ((size_t)u * cmax) * G * kRec, count, p.out + (size_t)u * G * kD, lane);
+    merge_unit<G>(p.partials + ((size_t)u * cmax) * G * kRec, count, p.out + (size_t)u * G * kD, lane,
+                  p.pout ? p.pout + (size_t)u * G * (kD + 2) : nullptr);
     if (lane == 0) p.counters[u] = 0u;
   };
   auto flush = [&](int u) {
@@ -255,6 +256,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     float lt = l + __shfl_xor_sync(0xffffffffu, l, 1);
     lt += __shfl_xor_sync(0xffffffffu, lt, 2);
     constexpr int kRec = kD + 4;
+    if (count == 1 && p.pout) {
+      if (live) {
+        float* po = p.pout + ((size_t)u * G + g) * (kD + 2);
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          po[8 * j + 2 * c] = acc[j][0] + acc[j][2];
+          po[8 * j + 2 * c + 1] = acc[j][1] + acc[j][3];
+        }
+        if (c == 0) { po[kD] = m; po[kD + 1] = lt; }
+      }
+      return;
+    }
     if (count == 1) {
       if (live) {
         const float inv = 1.f / lt;

@@ -67,8 +67,10 @@ struct DecodeArgs {
   const void* Vt;
   float scale;
   float* out;
+  float* pout = nullptr;  // token-shard partial state [U][G][d+2] instead of out
 };
 // kernel: 0 auto, 1 generic, 2 fast.  Returns launches, -1 launch error, -2 unsupported.
+int launch_merge_parts(int U, int G, int d, int P, const float* parts, float* out, cudaStream_t st);
 void set_decode_trace(void* buf);  // diagnostics (rotatek_debug_decode_trace)
 int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kernel,
                   cudaStream_t st);

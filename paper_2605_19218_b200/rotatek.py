@@ -69,9 +69,12 @@ def lib():
             L.rotatek_decode_attn_ex.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz,
                                                  i32, i32, vp]
             L.rotatek_select_topr.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp]
+            L.rotatek_decode_attn_partial.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz, vp]
+            L.rotatek_merge_partials.argtypes = [i32, i32, i32, i32, vp, vp, vp]
             for fn in ("rotatek_calibrate", "rotatek_compress_kv", "rotatek_compress_kv_ex",
                        "rotatek_decode_attn",
-                       "rotatek_decode_attn_ex", "rotatek_select_topr"):
+                       "rotatek_decode_attn_ex", "rotatek_select_topr", "rotatek_decode_attn_partial",
+                       "rotatek_merge_partials"):
                 getattr(L, fn).restype = ctypes.c_int
             L.rotatek_status_string.argtypes = [ctypes.c_int]
             L.rotatek_status_string.restype = ctypes.c_char_p
@@ -249,6 +252,39 @@ def decode_attn(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, R: torch
                                         _ptr(V_text) if M else None, float(scale), _ptr(out),
                                         _ptr(ws), ws.numel(), int(splits), int(kernel),
                                         _stream(stream)))
+    return out
+
+
+def decode_attn_partial(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, R: torch.Tensor,
+                        dmu: torch.Tensor | None, K_text: torch.Tensor | None = None,
+                        V_text: torch.Tensor | None = None, scale: float = 0.0,
+                        part: torch.Tensor | None = None, *, ws: torch.Tensor | None = None,
+                        stream=None) -> torch.Tensor:
+    """Alg. 2 over this rank's token shard -> un-normalised state part [U, G, d+2] f32
+    (acc[d] | m | l, base-2 logits; include/rotatek.h)."""
+    U, G, d = q.shape
+    N, r = K_comp.shape[1], K_comp.shape[2]
+    M = 0 if K_text is None else K_text.shape[1]
+    assert V.shape == (U, N, d) and R.shape == (U, d, r)
+    dims = make_dims(U, G, d, r, N, M, 0, _dtype_code(K_comp))
+    if part is None:
+        part = torch.empty((U, G, d + 2), dtype=torch.float32, device=q.device)
+    if ws is None:
+        ws = workspace(dims, OP_DECODE, q.device)
+    _check(lib().rotatek_decode_attn_partial(ctypes.byref(dims), _ptr(q), _ptr(K_comp), _ptr(V),
+                                             _ptr(R), _ptr(dmu), _ptr(K_text) if M else None,
+                                             _ptr(V_text) if M else None, float(scale), _ptr(part),
+                                             _ptr(ws), ws.numel(), _stream(stream)))
+    return part
+
+
+def merge_partials(parts: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """parts [P, U, G, d+2] f32 (token shards, shard-major) -> out [U, G, d] f32."""
+    P, U, G, d2 = parts.shape
+    d = d2 - 2
+    if out is None:
+        out = torch.empty((U, G, d), dtype=torch.float32, device=parts.device)
+    _check(lib().rotatek_merge_partials(U, G, d, P, _ptr(parts), _ptr(out), _stream(stream)))
     return out
 
 

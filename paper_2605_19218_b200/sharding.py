@@ -8,6 +8,11 @@ rank's share of a batch is a contiguous unit range, i.e. a pointer offset into t
   the global units [r*U, (r+1)*U).
 * strong scaling: a fixed global batch of U units is split into contiguous ranges of
   ceil(U / world) (the last rank may get fewer, ranks beyond U get none).
+* token sharding (U < world, e.g. Qwen b1 with 4 units on 8 GPUs): every
+  rank holds all units but only its contiguous slice of the visual (and text) tokens; it
+  runs Alg. 2 over its slice (rotatek_decode_attn_partial), the [U, G, d+2] states are
+  all-gathered (the one collective: NCCL all_gather_into_tensor) and merged
+  (rotatek_merge_partials) -- the exact online-softmax merge of App. C.
 """
 from __future__ import annotations
 
@@ -34,3 +39,25 @@ def max_over_ranks(value: float, group=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+def token_slice(n: int, world: int, rank: int) -> range:
+    """Balanced contiguous slice of n tokens for `rank` (sizes differ by at most one)."""
+    return range(n * rank // world, n * (rank + 1) // world)
+
+
+def decode_token_sharded(q, K_comp, V, R, dmu, K_text=None, V_text=None, scale=0.0, group=None):
+    """Token-sharded Alg. 2: this rank's cache shard -> the full output [U, G, d] on every
+    rank.  One all-gather of the [U, G, d+2] fp32 states, then the merge kernel."""
+    import torch
+    import torch.distributed as dist
+
+    from . import rotatek as rk
+    part = rk.decode_attn_partial(q, K_comp, V, R, dmu, K_text, V_text, scale)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if world == 1:
+        return rk.merge_partials(part[None])
+    parts = torch.empty((world * part.shape[0],) + tuple(part.shape[1:]), dtype=part.dtype,
+                        device=part.device)
+    dist.all_gather_into_tensor(parts, part, group=group)
+    return rk.merge_partials(parts.view((world,) + tuple(part.shape)))

@@ -410,3 +410,45 @@ def test_compress_tensor_core(rk, r, h_kv, n_vis):
         assert np.all(np.abs(got - want) <= 2.0 ** -7 * np.abs(want) + 64 * 2.0 ** -24 * absdot)
         assert np.mean(got == want) > 0.995
     assert np.mean(to_np64(a) == to_np64(b)) > 0.995
+
+
+# ------------------------------------------------------------------ token-sharded decode (8(e))
+@pytest.mark.parametrize("name", ["llava_small", "qwen_small_r32", "qwen_small_r64", "odd_r", "toy"])
+@pytest.mark.parametrize("dtype", ["bf16", "f32"])
+def test_decode_token_shards_merge(rk, name, dtype):
+    """Alg. 2 over uneven token shards (rotatek_decode_attn_partial) merged by
+    rotatek_merge_partials equals the oracle decode of the whole cache (G-dec), and each
+    shard's state normalises to the oracle decode of that shard."""
+    import torch
+    cfg = SMALL[name].with_(dtype=dtype)
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, dtype)
+    q, V = w["q"].f64(), w["V"].f64()
+    M = cfg.n_text
+    Kx = w["Ktext"].f64() if M else None
+    Vx = w["Vtext"].f64() if M else None
+    ref = orc.decode(q, Kt, V, R, dmu, Kx, Vx)
+    N = cfg.n_vis
+    vcut = [0, N // 5, N // 5 + (N * 3) // 7, N]              # three uneven visual shards
+    xcut = [0, 0, M // 2, M] if M else [0, 0, 0, 0]           # text: none on shard 0
+    Rt = torch.from_numpy(R.astype(np.float32)).cuda()
+    dt = torch.from_numpy(dmu.astype(np.float32)).cuda()
+    qt = to_torch(w["q"])
+    parts = []
+    for s in range(3):
+        a, b = vcut[s], vcut[s + 1]
+        xa, xb = xcut[s], xcut[s + 1]
+        ks = _as_dev(Kt[:, a:b], dtype).contiguous()
+        vs = _as_dev(V[:, a:b], dtype).contiguous()
+        kx = _as_dev(Kx[:, xa:xb], dtype).contiguous() if xb > xa else None
+        vx = _as_dev(Vx[:, xa:xb], dtype).contiguous() if xb > xa else None
+        part = rk.decode_attn_partial(qt, ks, vs, Rt, dt, kx, vx)
+        torch.cuda.synchronize()
+        shard_ref = orc.decode(q, Kt[:, a:b], V[:, a:b], R, dmu,
+                               Kx[:, xa:xb] if xb > xa else None, Vx[:, xa:xb] if xb > xa else None)
+        pn = to_np64(part)
+        assert max_rel_err(pn[..., :-2] / pn[..., -1:], shard_ref) <= TOL[dtype]
+        parts.append(part)
+    out = rk.merge_partials(torch.stack(parts))
+    torch.cuda.synchronize()
+    assert max_rel_err(to_np64(out), ref) <= TOL[dtype]

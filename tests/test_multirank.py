@@ -85,3 +85,57 @@ def test_strong_units_cover_exactly():
             got = [u for r in range(world) for u in strong_units(total, r, world)]
             assert got == list(range(total))
     assert list(weak_units(4, 3)) == [12, 13, 14, 15]
+
+
+def _token_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from oracle import oracle as orc
+        from paper_2605_19218_b200.sharding import token_slice
+        rng = np.random.default_rng(11)       # every rank draws the same replicated inputs
+        U, G, d, r, N, M = 2, 3, 16, 4, 37, 6
+        qv = rng.standard_normal((U, G, d))
+        Kt = rng.standard_normal((U, N, r))
+        V = rng.standard_normal((U, N, d))
+        R = np.linalg.qr(rng.standard_normal((U, d, d)))[0][:, :, :r]
+        dmu = rng.standard_normal((U, d))
+        Kx = rng.standard_normal((U, M, d))
+        Vx = rng.standard_normal((U, M, d))
+        vs, xs = token_slice(N, world, rank), token_slice(M, world, rank)
+        part = orc.decode_partial(qv, Kt[:, vs.start:vs.stop], V[:, vs.start:vs.stop], R, dmu,
+                                  Kx[:, xs.start:xs.stop], Vx[:, xs.start:xs.stop])
+        t = torch.from_numpy(np.ascontiguousarray(part))
+        parts = torch.empty((world * t.shape[0],) + tuple(t.shape[1:]), dtype=t.dtype)
+        dist.all_gather_into_tensor(parts, t)
+        parts = parts.view((world,) + tuple(t.shape))
+        if rank == 0:
+            out = orc.merge_partials(parts.numpy())
+            ref = orc.decode(qv, Kt, V, R, dmu, Kx, Vx)
+            q.put(float(np.abs(out - ref).max()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_token_shards_merge_to_full_decode():
+    """Token sharding for U < P: each rank's Alg. 2 state over its token
+    slice, all-gathered and merged, equals the unsharded decode (exact re-association)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_token_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    assert q.get(timeout=10) <= 1e-12
+
+
+def test_token_slices_cover_exactly():
+    from paper_2605_19218_b200.sharding import token_slice
+    for n in (1, 7, 64, 2880):
+        for world in (1, 2, 3, 8):
+            got = [t for r in range(world) for t in token_slice(n, world, r)]
+            assert got == list(range(n))

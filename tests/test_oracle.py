@@ -273,6 +273,37 @@ def test_decode_full_rank_equals_standard_attention():
             np.testing.assert_allclose(out[u, g], ref, atol=1e-12)
 
 
+def test_partial_states_merge_to_brute_force_attention():
+    """Token-shard states (App. C online-softmax state) merged over any split
+    equal brute-force softmax attention over the whole cache (r = d, orthogonal R so that
+    the scores are standard attention; pins decode_partial / merge_partials independently
+    of orc.decode), and a single shard's state has l = sum 2^(z - max z) with m the max."""
+    rng = np.random.default_rng(23)
+    U, G, d, N, M = 2, 2, 8, 29, 4
+    K = rng.standard_normal((U, N, d))
+    V = rng.standard_normal((U, N, d))
+    Kx, Vx = rng.standard_normal((U, M, d)), rng.standard_normal((U, M, d))
+    q = rng.standard_normal((U, G, d))
+    R = np.stack([np.linalg.qr(rng.standard_normal((d, d)))[0] for _ in range(U)])
+    Kt = orc.compress(K, R)
+    for cuts, xcuts in [([0, 29], [0, 4]), ([0, 1, 29], [0, 4, 4]), ([0, 10, 11, 29], [0, 0, 1, 4])]:
+        parts = np.stack([orc.decode_partial(q, Kt[:, a:b], V[:, a:b], R, None,
+                                             Kx[:, xa:xb], Vx[:, xa:xb])
+                          for a, b, xa, xb in zip(cuts, cuts[1:], xcuts, xcuts[1:])])
+        out = orc.merge_partials(parts)
+        for u in range(U):
+            for g in range(G):
+                ref = _attn(q[u, g], np.vstack([K[u], Kx[u]]), np.vstack([V[u], Vx[u]]),
+                            1 / math.sqrt(d))
+                np.testing.assert_allclose(out[u, g], ref, atol=1e-12)
+    one = orc.decode_partial(q, Kt, V, R, None, Kx, Vx)
+    z = np.concatenate([np.einsum("gd,nd->gn", q[0], K[0]), np.einsum("gd,nd->gn", q[0], Kx[0])],
+                       axis=1) / math.sqrt(d) * math.log2(math.e)
+    np.testing.assert_allclose(one[0, :, -2], z.max(axis=1), atol=1e-12)
+    np.testing.assert_allclose(one[0, :, -1], np.exp2(z - z.max(axis=1, keepdims=True)).sum(axis=1),
+                               rtol=1e-12)
+
+
 def test_decode_single_token_and_zero_query():
     rng = np.random.default_rng(17)
     d, r = 8, 3

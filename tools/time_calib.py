@@ -16,6 +16,10 @@ for name, flags in [("fp32-jacobi+fp64-refine", rk.DEFAULT_FLAGS), ("fp64-jacobi
         cal = rk.calibrate(K, Qw, cfg.rank, flags)
         torch.cuda.synchronize(); t1 = time.perf_counter()
     info = cal["info"].cpu().numpy()
+    torch.cuda.synchronize(); t2 = time.perf_counter()
+    Kc = rk.compress_kv(K, cal["R"])
+    torch.cuda.synchronize(); t3 = time.perf_counter()
+    print(f"   compress: {1e3*(t3-t2):.3f} ms (host-timed)")
     print(f"{cfg.name} {name}: {1e3*(t1-t0):.2f} ms  info>0: {(info>0).sum()}  info<0: {(info<0).sum()}")
 
 from workload.gen import draw_v0
