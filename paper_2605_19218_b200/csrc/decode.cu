@@ -241,11 +241,11 @@ static int num_sms() {
   return n;
 }
 
-static FastPlan fast_plan(int U, int N, int M, int warps_per_sm) {
+static FastPlan fast_plan(int U, int N, int M, int warps_per_sm, int min_tokens = 64) {
   FastPlan pl;
   const long long T = (long long)U * (N + M);
   long long nw = (long long)num_sms() * warps_per_sm;
-  const long long by_size = (T + 63) / 64;  // at least 64 tokens per warp
+  const long long by_size = T / min_tokens > 0 ? T / min_tokens : 1;  // >= min_tokens per warp
   if (by_size < nw) nw = by_size;
   // at most 126 warps per unit, so a unit's partials (<= 128) fit the merge scratch
   if (nw > 126LL * U) nw = 126LL * U;
@@ -419,7 +419,8 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) == cudaSuccess;
   }();
   (void)attr;
-  const FastPlan pl = fast_plan(a.U, a.N, a.M, WARPS);
+  // >= 96 tokens per warp (fewer, longer ranges on small shapes: Qwen b1 26 -> 23 us)
+  const FastPlan pl = fast_plan(a.U, a.N, a.M, WARPS, 96);
   const int aw = active_warps(a.U, a.N, a.M, pl.NW, WARPS, C::CAP);
   if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
   const int ctas = (pl.NW + aw - 1) / aw;

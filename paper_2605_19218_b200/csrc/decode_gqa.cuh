@@ -99,8 +99,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   const long long Ttot = L * p.U;
   RK_TRACE(0, gtime());
   int uA, nu;
-  cta_units(Ttot, NW, p.aw, blockIdx.x, L, uA, nu);
-  const long long a = range_start(Ttot, gw, NW), b = range_start(Ttot, gw + 1, NW);
+  // equal split (rounding the split points to the tile grid removes the ~7% box over-read at
+  // range ends but measured no faster: Split av/ax = C::TT/C::TX)
+  const Split sp{Ttot, L, NW, N, 1, 1};
+  cta_units(sp, p.aw, blockIdx.x, uA, nu);
+  const long long a = sp.start(gw), b = sp.start(gw + 1);
   const bool active = w < p.aw && gw < NW && a < b;
   const uint64_t pol = policy_evict_first();
   if (active && lane == 0) {
@@ -251,7 +254,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   };
   auto flush = [&](int u) {
     const long long x0 = (long long)u * L, x1 = x0 + L - 1;
-    const int first = warp_of(x0, Ttot, NW), last = warp_of(x1, Ttot, NW);
+    const int first = sp.warp_of(x0), last = sp.warp_of(x1);
     const int count = last - first + 1;
     float lt = l + __shfl_xor_sync(0xffffffffu, l, 1);
     lt += __shfl_xor_sync(0xffffffffu, lt, 2);
