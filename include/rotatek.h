@@ -167,6 +167,15 @@ rotatek_status rotatek_compress_kv(const rotatek_dims* dims, const void* K, cons
 rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dims, const void* K, const float* R,
                                       void* K_comp, uint32_t flags, rotatek_stream_t stream);
 
+/* Same with a shared rotation (NEXT-3, offline calibrated variant): R is
+ * [r_units, d, r] and unit u uses R[u % r_units] (r_units = H_kv: one rotation per kv head,
+ * reused across the batch b, since u = b*H_kv + h).  r_units must divide units; 0 means
+ * one rotation per unit (== rotatek_compress_kv_ex).  Errors as rotatek_compress_kv_ex,
+ * plus DIMS for a bad r_units. */
+rotatek_status rotatek_compress_kv_ex2(const rotatek_dims* dims, int32_t r_units, const void* K,
+                                       const float* R, void* K_comp, uint32_t flags,
+                                       rotatek_stream_t stream);
+
 /*
  * Alg. 2 for all U*G query heads in one launch:
  *   q~ = q R_r ; b = q . dmu
@@ -204,6 +213,50 @@ rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dims, const void* q,
                                       float softmax_scale, float* out, void* workspace,
                                       size_t workspace_bytes, int32_t splits, int32_t kernel,
                                       rotatek_stream_t stream);
+
+/* Same with a shared rotation: R [r_units, d, r] and dmu [r_units, d]; unit u uses index
+ * u % r_units (r_units divides units; 0 = one per unit).  See rotatek_compress_kv_ex2. */
+rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dims, int32_t r_units, const void* q,
+                                       const void* K_comp, const void* V, const float* R,
+                                       const float* dmu, const void* K_text, const void* V_text,
+                                       float softmax_scale, float* out, void* workspace,
+                                       size_t workspace_bytes, int32_t splits, int32_t kernel,
+                                       rotatek_stream_t stream);
+
+/*
+ * Calibration statistics, accumulated on the device (NEXT-3 offline calibrated rotation,
+ * P:588 "precomputed from calibration data and reused across samples"; and the
+ * calibration half of token-sharded prefill).  The fp64 state holds the sums
+ * behind Alg. 1 l.1-5, one entry of ROTATEK_STATE_DOUBLES(d) doubles per state unit s:
+ *     S [d][d] = sum_n k_n k_n^T  |  colsum [d] = sum_n k_n  |
+ *     sigma2 [d] = sum over query windows of q_j^2 (Q_W, pooled as in rotatek_calibrate) |
+ *     count = number of tokens  |  one pad double
+ * rotatek_calib_accumulate ADDS unit u's keys K[u] (and window Qw[u] if QUERY_WEIGHT and
+ * q_window > 0) into entry u % state_units (state_units divides units; ascending u, so the
+ * result is deterministic).  Zero the state once before the first call.  For token
+ * sharding each rank accumulates its slice and the states are all-reduced (summed).
+ * Errors: NULL, DIMS (also: bad state_units), ALIGN, WORKSPACE (size = rotatek_workspace_
+ * bytes(dims, CALIBRATE)), UNSUPPORTED (d > 128), CUDA.
+ */
+#define ROTATEK_STATE_DOUBLES(d) ((size_t)(d) * (size_t)(d) + 2 * (size_t)(d) + 2)
+rotatek_status rotatek_calib_accumulate(const rotatek_dims* dims, uint32_t flags, const void* K,
+                                        const void* Qw, int32_t state_units, double* state,
+                                        void* workspace, size_t workspace_bytes,
+                                        rotatek_stream_t stream);
+
+/*
+ * Alg. 1 from an accumulated state (dims->units = number of state entries; n_vis,
+ * q_window ignored): mu = colsum / count (CENTER, else 0), C = S - count mu mu^T,
+ * C_q = (sigma sigma^T) (.) C with sigma = sqrt(sigma2) (QUERY_WEIGHT, else 1), then the
+ * eigensolver, top-r select and delta_mu exactly as rotatek_calibrate (same outputs,
+ * layouts, flags EIG_FP64, errors; workspace: rotatek_workspace_bytes with n_vis = 1).
+ */
+rotatek_status rotatek_calibrate_from_state(const rotatek_dims* dims, uint32_t flags,
+                                            const double* state, float* R, float* dmu,
+                                            float* eigvals, uint32_t* keep_mask,
+                                            int32_t* keep_idx, float* R_full, int32_t* info,
+                                            void* workspace, size_t workspace_bytes,
+                                            rotatek_stream_t stream);
 
 /*
  * Token-sharded decode (when there are fewer units than GPUs, the token axis

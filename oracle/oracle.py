@@ -187,6 +187,58 @@ def calibrate(K, Qw, r, center=True, query_weight=True, tol=JACOBI_TOL,
     return out
 
 
+def state_doubles(d: int) -> int:
+    return d * d + 2 * d + 2
+
+
+def calib_state(K, Qw, state_units, query_weight=True, state=None) -> np.ndarray:
+    """NEXT-3 / calibrate-side token sharding: the sums behind Alg. 1 l.1-5 per
+    state entry s, adding every unit u with u % state_units == s (ascending u):
+        S = sum_n k_n k_n^T, colsum = sum_n k_n, sigma2_j = sum_window q_j^2, count = #tokens.
+    Returns (or adds into) [state_units, d*d + 2d + 2] fp64 (layout of rotatek_calib_accumulate)."""
+    K = _f64(K)
+    U, N, d = K.shape
+    if state is None:
+        state = np.zeros((state_units, state_doubles(d)))
+    for u in range(U):
+        s = u % state_units
+        S = state[s, : d * d].reshape(d, d)
+        S += K[u].T @ K[u]
+        state[s, d * d: d * d + d] += K[u].sum(axis=0)
+        if query_weight and Qw is not None and Qw.shape[2] > 0:
+            state[s, d * d + d: d * d + 2 * d] += (_f64(Qw[u]) ** 2).sum(axis=(0, 1))
+        state[s, d * d + 2 * d] += N
+    return state
+
+
+def calibrate_from_state(state, r, center=True, query_weight=True, tol=JACOBI_TOL,
+                         max_sweeps=JACOBI_MAX_SWEEPS) -> dict:
+    """Alg. 1 l.1-6 from pooled sums: mu = colsum / count, C = S - count mu mu^T,
+    C_q = (sigma sigma^T) (.) C with sigma = sqrt(sigma2) (pooled as Q4) or 1,
+    then the exact eigendecomposition, top-r select and delta_mu of calibrate()."""
+    state = _f64(state)
+    nS = state.shape[0]
+    d = int(round((-2 + np.sqrt(4 + 4 * (state.shape[1] - 2))) / 2))
+    out = dict(mu=np.empty((nS, d)), Cq=np.empty((nS, d, d)), lam=np.empty((nS, d)),
+               R=np.empty((nS, d, r)), dmu=np.empty((nS, d)),
+               mask=np.zeros((nS, (d + 31) // 32), dtype=np.uint32), idx=np.zeros((nS, r), np.int32))
+    for s in range(nS):
+        S = state[s, : d * d].reshape(d, d)
+        col = state[s, d * d: d * d + d]
+        n = state[s, d * d + 2 * d]
+        mu = col / n if center else np.zeros(d)
+        C = S - n * np.outer(mu, mu)
+        sig = np.sqrt(state[s, d * d + d: d * d + 2 * d]) if query_weight else np.ones(d)
+        Cq = np.outer(sig, sig) * C
+        Cq = 0.5 * (Cq + Cq.T)
+        lam, V, _ = jacobi(Cq, tol, max_sweeps)
+        mask, idx = select_topr(lam, r)
+        Rr, dmu = rotation(V, idx, mu)
+        out["mu"][s], out["Cq"][s], out["lam"][s] = mu, Cq, lam
+        out["R"][s], out["dmu"][s], out["mask"][s], out["idx"][s] = Rr, dmu, mask, idx
+    return out
+
+
 def compress(K, R) -> np.ndarray:
     """K~ = K R_r in fp64 (Alg. 1 l.14), before the quantisation point."""
     K = _f64(K)

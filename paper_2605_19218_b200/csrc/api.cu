@@ -155,7 +155,70 @@ rotatek_status rotatek_calibrate_subspace(const rotatek_dims* dm, uint32_t flags
   return ROTATEK_OK;
 }
 
-rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dm, const void* K, const float* R,
+rotatek_status rotatek_calib_accumulate(const rotatek_dims* dm, uint32_t flags, const void* K,
+                                        const void* Qw, int32_t state_units, double* state,
+                                        void* workspace, size_t workspace_bytes, rotatek_stream_t stream) {
+  g_launches = 0;
+  rotatek_status s = check_dims(dm);
+  if (s != ROTATEK_OK) return s;
+  const int U = dm->units, G = dm->group, d = dm->head_dim, N = dm->n_vis, W = dm->q_window;
+  const bool bf16 = dm->dtype == ROTATEK_BF16;
+  const bool weight = (flags & ROTATEK_QUERY_WEIGHT) && W > 0;
+  if (!K || !state) return fail(ROTATEK_ERR_NULL, "K and state are required");
+  if (W > 0 && !Qw) return fail(ROTATEK_ERR_DIMS, "Qw is NULL but q_window > 0");
+  if (state_units < 1 || U % state_units != 0) return fail(ROTATEK_ERR_DIMS, "state_units must divide units");
+  if (d > 128) return fail(ROTATEK_ERR_UNSUPPORTED, "calibrate supports head_dim <= 128");
+  const void* ptrs[] = {K, Qw, state, workspace};
+  for (const void* p : ptrs)
+    if (p && !aligned16(p)) return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
+  rk::CalibWs ws;
+  const size_t need = rk::calib_ws_layout(U, d, N, true, workspace, &ws);
+  if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int n = 0;
+  if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
+  const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::cov_tc_supported(d, bf16);
+  if ((s = launched(tc ? rk::launch_cov_tc(U, N, true, K, ws, st, /*allow_fused=*/false)
+                       : rk::launch_cov(U, N, d, bf16, K, ws, st),
+                    &n)))
+    return s;
+  if ((s = launched(rk::launch_state_accumulate(U, N, d, state_units, weight, ws, state, st), &n))) return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
+rotatek_status rotatek_calibrate_from_state(const rotatek_dims* dm, uint32_t flags, const double* state,
+                                            float* R, float* dmu, float* eigvals, uint32_t* keep_mask,
+                                            int32_t* keep_idx, float* R_full, int32_t* info, void* workspace,
+                                            size_t workspace_bytes, rotatek_stream_t stream) {
+  g_launches = 0;
+  rotatek_status s = check_dims(dm);
+  if (s != ROTATEK_OK) return s;
+  const int U = dm->units, d = dm->head_dim, r = dm->rank;
+  const bool bf16 = dm->dtype == ROTATEK_BF16;
+  const bool weight = (flags & ROTATEK_QUERY_WEIGHT) != 0;
+  const bool center = (flags & ROTATEK_CENTER) != 0;
+  const bool fp64 = !bf16 || (flags & ROTATEK_EIG_FP64);
+  if (!state || !R || !dmu) return fail(ROTATEK_ERR_NULL, "state, R and dmu are required");
+  if (d > 128) return fail(ROTATEK_ERR_UNSUPPORTED, "calibrate supports head_dim <= 128");
+  const void* ptrs[] = {state, R, dmu, eigvals, keep_mask, keep_idx, R_full, info, workspace};
+  for (const void* p : ptrs)
+    if (p && !aligned16(p)) return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
+  rk::CalibWs ws;
+  const size_t need = rk::calib_ws_layout(U, d, 1, true, workspace, &ws);
+  if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int n = 0;
+  if ((s = launched(rk::launch_state_finalize(U, d, center, weight, state, ws, st), &n))) return s;
+  if ((s = launched(rk::launch_jacobi(U, d, fp64, ws, st), &n))) return s;
+  if ((s = launched(rk::launch_select_gather(U, d, r, /*fp64_vecs=*/true, bf16, center, ws, R, dmu, eigvals,
+                                             keep_mask, keep_idx, R_full, info, st), &n)))
+    return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
+rotatek_status rotatek_compress_kv_ex2(const rotatek_dims* dm, int32_t r_units, const void* K, const float* R,
                                       void* K_comp, uint32_t flags, rotatek_stream_t stream) {
   g_launches = 0;
   rotatek_status s = check_dims(dm);
@@ -164,18 +227,25 @@ rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dm, const void* K, con
   if (!aligned16(K) || !aligned16(R) || !aligned16(K_comp))
     return fail(ROTATEK_ERR_ALIGN, "pointer not 16-byte aligned");
   const int d = dm->head_dim, r = dm->rank;
+  if (r_units < 0 || (r_units > 0 && dm->units % r_units != 0))
+    return fail(ROTATEK_ERR_DIMS, "r_units must divide units (0: one rotation per unit)");
   const bool bf16 = dm->dtype == ROTATEK_BF16;
   const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::compress_tc_supported(d, r, bf16);
   if (!tc && ((size_t)d * r + 64 * (size_t)d) * 4 > 227 * 1024)
     return fail(ROTATEK_ERR_UNSUPPORTED, "compress: d*r too large");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int n = 0;
-  if ((s = launched(tc ? rk::launch_compress_tc(dm->units, dm->n_vis, r, K, R, K_comp, st)
-                       : rk::launch_compress(dm->units, dm->n_vis, d, r, bf16, K, R, K_comp, st),
+  if ((s = launched(tc ? rk::launch_compress_tc(dm->units, dm->n_vis, r, K, R, K_comp, st, r_units)
+                       : rk::launch_compress(dm->units, dm->n_vis, d, r, bf16, K, R, K_comp, st, r_units),
                     &n)))
     return s;
   g_launches = n;
   return ROTATEK_OK;
+}
+
+rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dm, const void* K, const float* R,
+                                      void* K_comp, uint32_t flags, rotatek_stream_t stream) {
+  return rotatek_compress_kv_ex2(dm, 0, K, R, K_comp, flags, stream);
 }
 
 rotatek_status rotatek_compress_kv(const rotatek_dims* dm, const void* K, const float* R,
@@ -183,7 +253,7 @@ rotatek_status rotatek_compress_kv(const rotatek_dims* dm, const void* K, const 
   return rotatek_compress_kv_ex(dm, K, R, K_comp, 0u, stream);
 }
 
-rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dm, const void* q, const void* K_comp,
+rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dm, int32_t r_units, const void* q, const void* K_comp,
                                       const void* V, const float* R, const float* dmu,
                                       const void* K_text, const void* V_text, float softmax_scale,
                                       float* out, void* workspace, size_t workspace_bytes,
@@ -202,6 +272,8 @@ rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dm, const void* q, con
                                            workspace, &ws);
   if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
   if (kernel < 0 || kernel > 3) return fail(ROTATEK_ERR_DIMS, "kernel must be 0, 1, 2 or 3");
+  if (r_units < 0 || (r_units > 0 && dm->units % r_units != 0))
+    return fail(ROTATEK_ERR_DIMS, "r_units must divide units (0: one rotation per unit)");
   rk::DecodeArgs a;
   a.U = dm->units; a.G = dm->group; a.d = dm->head_dim; a.r = dm->rank; a.N = dm->n_vis; a.M = M;
   a.bf16 = dm->dtype == ROTATEK_BF16;
@@ -209,11 +281,21 @@ rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dm, const void* q, con
   a.Kt = M > 0 ? K_text : nullptr; a.Vt = M > 0 ? V_text : nullptr;
   a.scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf((float)dm->head_dim);
   a.out = out;
+  a.nR = r_units;
   int n = 0;
   if ((s = launched(rk::launch_decode(a, ws, splits, kernel, reinterpret_cast<cudaStream_t>(stream)), &n)))
     return s;
   g_launches = n;
   return ROTATEK_OK;
+}
+
+rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dm, const void* q, const void* K_comp,
+                                      const void* V, const float* R, const float* dmu,
+                                      const void* K_text, const void* V_text, float softmax_scale,
+                                      float* out, void* workspace, size_t workspace_bytes,
+                                      int32_t splits, int32_t kernel, rotatek_stream_t stream) {
+  return rotatek_decode_attn_ex2(dm, 0, q, K_comp, V, R, dmu, K_text, V_text, softmax_scale, out, workspace,
+                                 workspace_bytes, splits, kernel, stream);
 }
 
 rotatek_status rotatek_decode_attn(const rotatek_dims* dm, const void* q, const void* K_comp,

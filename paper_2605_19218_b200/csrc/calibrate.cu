@@ -986,6 +986,93 @@ int launch_select_only(int U, int d, int r, const float* lam, uint32_t* mask, in
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// ============================================================== calibration statistics state
+// NEXT-3 (offline calibrated rotation) and calibrate-side token sharding:
+// the sums behind Alg. 1 l.1-5 kept in fp64 per state entry s (stride d*d + 2d + 2 doubles):
+//   S [d][d] = sum k k^T | colsum [d] = sum k | sigma2 [d] = sum q^2 over the windows | count
+// Unit u adds into entry u % nS (nS = H_kv pools a batch of calibration samples per kv head;
+// nS = U keeps one entry per unit, e.g. for an all-reduce across token shards).  Units of
+// one entry are added in ascending u (deterministic).
+__global__ void __launch_bounds__(256) state_accumulate_kernel(int U, int N, int d, int nS, int parts, bool weight,
+                                                               const double* __restrict__ covpart,
+                                                               const double* __restrict__ colpart,
+                                                               const double* __restrict__ sigma,
+                                                               double* __restrict__ state) {
+  const int sidx = blockIdx.x;
+  const size_t stride = (size_t)d * d + 2 * d + 2;
+  double* S = state + (size_t)sidx * stride;
+  double* col = S + (size_t)d * d;
+  double* sg2 = col + d;
+  // rows of S split over blockIdx.y (enough CTAs when nS is small)
+  const int rows = (d + gridDim.y - 1) / gridDim.y;
+  const int e0 = blockIdx.y * rows * d, e1 = min(d, (int)(blockIdx.y + 1) * rows) * d;
+  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int i = e / d, j = e % d, a = min(i, j), b = max(i, j);  // partials hold the upper tiles
+    double acc = S[e];
+    for (int u = sidx; u < U; u += nS)
+      for (int p = 0; p < parts; ++p) acc += covpart[((size_t)u * parts + p) * d * d + (size_t)a * d + b];
+    S[e] = acc;
+  }
+  if (blockIdx.y == 0) {
+    for (int j = threadIdx.x; j < d; j += blockDim.x) {
+      double c = col[j], q = sg2[j];
+      for (int u = sidx; u < U; u += nS) {
+        for (int p = 0; p < parts; ++p) c += colpart[((size_t)u * parts + p) * d + j];
+        if (weight) { const double sv = sigma[(size_t)u * d + j]; q = fma(sv, sv, q); }
+      }
+      col[j] = c;
+      sg2[j] = q;
+    }
+    if (threadIdx.x == 0) {
+      double n = 0.0;
+      for (int u = sidx; u < U; u += nS) n += (double)N;
+      sg2[d] += n;  // count
+    }
+  }
+}
+
+int launch_state_accumulate(int U, int N, int d, int nS, bool weight, const CalibWs& ws, double* state,
+                            cudaStream_t st) {
+  state_accumulate_kernel<<<dim3(nS, 8), 256, 0, st>>>(U, N, d, nS, ws.parts, weight, ws.covpart, ws.colpart,
+                                                       ws.sigma, state);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+// mu = colsum / count ; C = S - count mu mu^T ; C_q = (sigma sigma^T) (.) C with
+// sigma = sqrt(sigma2) (weight) or 1 -> ws.cq, ws.mu (the inputs of the eigensolver + select)
+__global__ void __launch_bounds__(256) state_finalize_kernel(int d, bool center, bool weight,
+                                                             const double* __restrict__ state,
+                                                             double* __restrict__ cq, double* __restrict__ mu_out) {
+  extern __shared__ double sh[];  // mu [d], sigma [d]
+  double* sh_sig = sh + d;
+  const int s = blockIdx.x;
+  const size_t stride = (size_t)d * d + 2 * d + 2;
+  const double* S = state + (size_t)s * stride;
+  const double* col = S + (size_t)d * d;
+  const double* sg2 = col + d;
+  const double n = sg2[d];
+  for (int j = threadIdx.x; j < d; j += blockDim.x) {
+    const double m = (center && n > 0.0) ? col[j] / n : 0.0;
+    sh[j] = m;
+    if (blockIdx.y == 0) mu_out[(size_t)s * d + j] = m;
+    sh_sig[j] = weight ? sqrt(sg2[j]) : 1.0;
+  }
+  __syncthreads();
+  const int rows = (d + gridDim.y - 1) / gridDim.y;
+  const int e0 = blockIdx.y * rows * d, e1 = min(d, (int)(blockIdx.y + 1) * rows) * d;
+  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+    const int i = e / d, j = e % d, a = min(i, j), b = max(i, j);
+    const double c = S[(size_t)a * d + b] - n * sh[a] * sh[b];
+    cq[(size_t)s * d * d + e] = sh_sig[a] * sh_sig[b] * c;
+  }
+}
+
+int launch_state_finalize(int nS, int d, bool center, bool weight, const double* state, const CalibWs& ws,
+                          cudaStream_t st) {
+  state_finalize_kernel<<<dim3(nS, 8), 256, 2 * d * sizeof(double), st>>>(d, center, weight, state, ws.cq, ws.mu);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 // ============================================================== workspace layout
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 

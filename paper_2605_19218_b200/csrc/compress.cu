@@ -15,14 +15,14 @@ constexpr int kCmpTok = 64;
 template <typename T>
 __global__ void __launch_bounds__(256) compress_kernel(int N, int d, int r, const T* __restrict__ K,
                                                        const float* __restrict__ R,
-                                                       T* __restrict__ Kc) {
+                                                       T* __restrict__ Kc, int nR) {
   extern __shared__ __align__(16) float csm[];
   float* Rs = csm;               // [d][r]
   float* Ks = csm + d * r;       // [kCmpTok][d]
   const int u = blockIdx.y, t0 = blockIdx.x * kCmpTok;
   const int tn = min(kCmpTok, N - t0);
   const int tid = threadIdx.x;
-  const float* Ru = R + (size_t)u * d * r;
+  const float* Ru = R + (size_t)(u % nR) * d * r;  // nR < U: a shared (offline) rotation
   for (int e = tid; e < d * r; e += blockDim.x) Rs[e] = Ru[e];
   const T* Ku = K + ((size_t)u * N + t0) * d;
   for (int e = tid; e < tn * d; e += blockDim.x) Ks[e] = Elem<T>::to_f(Ku[e]);
@@ -47,16 +47,17 @@ __global__ void __launch_bounds__(256) compress_kernel(int N, int d, int r, cons
 }
 
 int launch_compress(int U, int N, int d, int r, bool bf16, const void* K, const float* R,
-                    void* Kc, cudaStream_t st) {
+                    void* Kc, cudaStream_t st, int nR) {
+  if (nR <= 0) nR = U;
   dim3 grid((N + kCmpTok - 1) / kCmpTok, U);
   size_t sm = ((size_t)d * r + (size_t)kCmpTok * d) * sizeof(float);
   if (bf16) {
     cudaFuncSetAttribute(compress_kernel<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     compress_kernel<__nv_bfloat16><<<grid, 256, sm, st>>>(N, d, r, (const __nv_bfloat16*)K, R,
-                                                         (__nv_bfloat16*)Kc);
+                                                         (__nv_bfloat16*)Kc, nR);
   } else {
     cudaFuncSetAttribute(compress_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    compress_kernel<float><<<grid, 256, sm, st>>>(N, d, r, (const float*)K, R, (float*)Kc);
+    compress_kernel<float><<<grid, 256, sm, st>>>(N, d, r, (const float*)K, R, (float*)Kc, nR);
   }
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }

@@ -44,7 +44,7 @@ __device__ __forceinline__ uint16_t bf16_bits_rn(float x) {
 template <int RK>
 __global__ void __launch_bounds__(kThreads, 1) compress_tc_kernel(const __grid_constant__ CUtensorMap tmap, int N,
                                                                   int parts, const float* __restrict__ R,
-                                                                  __nv_bfloat16* __restrict__ Kc) {
+                                                                  __nv_bfloat16* __restrict__ Kc, int nR) {
   using C = CmpCfg<RK>;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(kThreads, 1) compress_tc_kernel(const __grid_c
   const int nt = t_hi - t_lo;
 
   // ---- B = R^T split into hi/mid/lo bf16, K-major with the 128-byte swizzle
-  const float* Ru = R + (size_t)u * kDc * RK;
+  const float* Ru = R + (size_t)(u % nR) * kDc * RK;  // nR < U: a shared (offline) rotation
   for (int e = threadIdx.x; e < kDc * RK; e += blockDim.x) {
     const int ch = e / RK, n = e % RK;   // coalesced read of R[ch][n]
     const float x = Ru[e];
@@ -182,7 +182,8 @@ bool compress_tc_supported(int d, int r, bool bf16) {
 }
 
 template <int RK>
-static int launch_compress_tc_r(int U, int N, const void* K, const float* R, void* Kc, cudaStream_t st) {
+static int launch_compress_tc_r(int U, int N, const void* K, const float* R, void* Kc, cudaStream_t st,
+                                int nR) {
   using C = CmpCfg<RK>;
   CUtensorMap map;
   if (!encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTM, 128)) return -2;
@@ -196,16 +197,18 @@ static int launch_compress_tc_r(int U, int N, const void* K, const float* R, voi
   if (parts > ntiles) parts = ntiles;
   if (parts < 1) parts = 1;
   dim3 grid(parts, U);
-  compress_tc_kernel<RK><<<grid, kThreads, C::SMEM, st>>>(map, N, parts, R, static_cast<__nv_bfloat16*>(Kc));
+  compress_tc_kernel<RK><<<grid, kThreads, C::SMEM, st>>>(map, N, parts, R, static_cast<__nv_bfloat16*>(Kc),
+                                                          nR > 0 ? nR : U);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
-int launch_compress_tc(int U, int N, int r, const void* K, const float* R, void* Kc, cudaStream_t st) {
+int launch_compress_tc(int U, int N, int r, const void* K, const float* R, void* Kc, cudaStream_t st,
+                       int nR) {
   switch (r) {
-    case 16: return launch_compress_tc_r<16>(U, N, K, R, Kc, st);
-    case 32: return launch_compress_tc_r<32>(U, N, K, R, Kc, st);
-    case 64: return launch_compress_tc_r<64>(U, N, K, R, Kc, st);
-    case 128: return launch_compress_tc_r<128>(U, N, K, R, Kc, st);
+    case 16: return launch_compress_tc_r<16>(U, N, K, R, Kc, st, nR);
+    case 32: return launch_compress_tc_r<32>(U, N, K, R, Kc, st, nR);
+    case 64: return launch_compress_tc_r<64>(U, N, K, R, Kc, st, nR);
+    case 128: return launch_compress_tc_r<128>(U, N, K, R, Kc, st, nR);
   }
   return -2;
 }

@@ -239,7 +239,8 @@ bool encode_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64
 
 bool cov_tc_supported(int d, bool bf16) { return bf16 && d == kDc && get_encode() != nullptr; }
 
-int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, cudaStream_t st) {
+int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, cudaStream_t st,
+                  bool allow_fused) {
   CUtensorMap map;
   if (!encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTK, 128)) return -2;
   static bool attr = [] {
@@ -249,7 +250,7 @@ int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, c
   dim3 grid(ws.parts, U);
   // parts == 1: the kernel also finalizes (mu, C = S - N mu mu^T, C_q) -- no finalize launch
   cov_tc_kernel<<<grid, kThreads, kSmem, st>>>(map, N, ws.parts, ws.covpart, ws.colpart, ws.sigma, ws.cq,
-                                               ws.mu, center, ws.parts == 1);
+                                               ws.mu, center, allow_fused && ws.parts == 1);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

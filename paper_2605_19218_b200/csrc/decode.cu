@@ -50,6 +50,7 @@ struct DecodeParams {
   unsigned long long* trace = nullptr;  // diagnostics: [NW][8] globaltimer stamps (or null)
   int aw = 0;                           // active (streaming) warps per CTA (<= WARPS)
   float* pout = nullptr;                // partial-state output [U][G][d+2] (token shards) or null
+  int nR = 0;                           // unit u uses R[u % nR], dmu[u % nR]
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -102,7 +103,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) decode_generic_kernel(DecodePa
   const T* q = static_cast<const T*>(p.q) + (size_t)u * G * d;
   for (int e = tid; e < G * d; e += blockDim.x) qs[e] = Elem<T>::to_f(q[e]);
   __syncthreads();
-  const float* Ru = p.R + (size_t)u * d * r;
+  const float* Ru = p.R + (size_t)(u % p.nR) * d * r;
   for (int e = tid; e < G * r; e += blockDim.x) {
     const int g = e / r, k = e % r;
     float s = 0.f;
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) decode_generic_kernel(DecodePa
   for (int g = w; g < G; g += kGenWarps) {
     float s = 0.f;
     if (p.dmu)
-      for (int i = lane; i < d; i += 32) s = fmaf(qs[g * d + i], p.dmu[(size_t)u * d + i], s);
+      for (int i = lane; i < d; i += 32) s = fmaf(qs[g * d + i], p.dmu[(size_t)(u % p.nR) * d + i], s);
     s = warp_sum(s);
     if (lane == 0) bias[g] = s * p.sl;
   }
@@ -311,7 +312,7 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
   const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout};
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout, a.nR > 0 ? a.nR : a.U};
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)) return -1;
   return 1;
 }
@@ -425,7 +426,7 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
   if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
   const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout};
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout, a.nR > 0 ? a.nR : a.U};
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, pl.cmax)) return -1;
   return 1;
 }
@@ -485,7 +486,8 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
   int S = splits > 0 ? splits : decode_max_splits(a.U, a.N, a.M);
   if (S > ws.max_splits) S = ws.max_splits;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, nullptr, 0, a.pout};
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, nullptr, 0, a.pout,
+                 a.nR > 0 ? a.nR : a.U};
   size_t sm = ((size_t)a.G * a.d + (size_t)a.G * a.r + a.G + 2 * kGenWarps * a.G +
                (size_t)kGenWarps * a.G * a.d) * sizeof(float);
   dim3 grid(S, a.U);

@@ -269,7 +269,8 @@ __device__ __forceinline__ void rotate_cols(const DecodeParams& p, int u, int cb
   static_assert(NR % QV == 0, "row block");
   constexpr int BATCH = NR < 32 ? NR : 32;
   const int j = lane % C4, r0 = lane / C4;
-  const float4* Rr = reinterpret_cast<const float4*>(p.R + (size_t)u * kD * RK + (size_t)r0 * NR * RK +
+  const int ur = u % p.nR;  // nR < U: a shared (offline calibrated) rotation per kv head
+  const float4* Rr = reinterpret_cast<const float4*>(p.R + (size_t)ur * kD * RK + (size_t)r0 * NR * RK +
                                                      cb * CW) + j;
   const T* qu = static_cast<const T*>(p.q) + (size_t)u * G * kD;
   float4 rv[BATCH];
@@ -281,7 +282,7 @@ __device__ __forceinline__ void rotate_cols(const DecodeParams& p, int u, int cb
     const uint4* qsrc = reinterpret_cast<const uint4*>(qu);
     uint4* qdst = reinterpret_cast<uint4*>(ent + E::OFF_Q);
     for (int e = lane; e < QCH; e += 32) qdst[e] = __ldg(qsrc + e);
-    const float4 dm = p.dmu ? __ldg(reinterpret_cast<const float4*>(p.dmu + (size_t)u * kD) + lane)
+    const float4 dm = p.dmu ? __ldg(reinterpret_cast<const float4*>(p.dmu + (size_t)ur * kD) + lane)
                             : make_float4(0.f, 0.f, 0.f, 0.f);
     float* be = reinterpret_cast<float*>(ent + E::OFF_B);
 #pragma unroll

@@ -39,9 +39,16 @@ int launch_sigma(int U, int G, int W, int d, bool bf16, bool weight, const void*
 int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws, cudaStream_t st);
 bool cov_tc_supported(int d, bool bf16);
 bool compress_tc_supported(int d, int r, bool bf16);
-int launch_compress_tc(int U, int N, int r, const void* K, const float* R, void* Kc, cudaStream_t st);
+int launch_compress_tc(int U, int N, int r, const void* K, const float* R, void* Kc, cudaStream_t st,
+                       int nR = 0);
 // parts == 1 also finalizes (writes cq and mu): the caller skips launch_finalize
-int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, cudaStream_t st);
+int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, cudaStream_t st,
+                  bool allow_fused = true);
+// calibration statistics state (rotatek_calib_accumulate / rotatek_calibrate_from_state)
+int launch_state_accumulate(int U, int N, int d, int nS, bool weight, const CalibWs& ws, double* state,
+                            cudaStream_t st);
+int launch_state_finalize(int nS, int d, bool center, bool weight, const double* state, const CalibWs& ws,
+                          cudaStream_t st);
 int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st);
 int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st);
 int launch_select_gather(int U, int d, int r, bool fp64_vecs, bool bf16x2, bool center,
@@ -53,7 +60,7 @@ int launch_subspace(int U, int d, int k, int iters, double eps, bool center, con
 int launch_select_only(int U, int d, int r, const float* lam, uint32_t* mask, int32_t* idx,
                        int32_t* info, cudaStream_t st);
 int launch_compress(int U, int N, int d, int r, bool bf16, const void* K, const float* R,
-                    void* Kc, cudaStream_t st);
+                    void* Kc, cudaStream_t st, int nR = 0);
 
 struct DecodeArgs {
   int U, G, d, r, N, M;
@@ -68,6 +75,7 @@ struct DecodeArgs {
   float scale;
   float* out;
   float* pout = nullptr;  // token-shard partial state [U][G][d+2] instead of out
+  int nR = 0;             // distinct rotations: unit u uses R[u % nR], dmu[u % nR] (0: nR = U)
 };
 // kernel: 0 auto, 1 generic, 2 fast.  Returns launches, -1 launch error, -2 unsupported.
 int launch_merge_parts(int U, int G, int d, int P, const float* parts, float* out, cudaStream_t st);

@@ -70,11 +70,18 @@ def lib():
                                                  i32, i32, vp]
             L.rotatek_select_topr.argtypes = [i32, i32, i32, vp, vp, vp, vp, vp]
             L.rotatek_decode_attn_partial.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz, vp]
+            L.rotatek_decode_attn_ex2.argtypes = [dp, i32, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz,
+                                                  i32, i32, vp]
+            L.rotatek_compress_kv_ex2.argtypes = [dp, i32, vp, vp, vp, u32, vp]
+            L.rotatek_calib_accumulate.argtypes = [dp, u32, vp, vp, i32, vp, vp, sz, vp]
+            L.rotatek_calibrate_from_state.argtypes = [dp, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                                       sz, vp]
             L.rotatek_merge_partials.argtypes = [i32, i32, i32, i32, vp, vp, vp]
             for fn in ("rotatek_calibrate", "rotatek_compress_kv", "rotatek_compress_kv_ex",
                        "rotatek_decode_attn",
                        "rotatek_decode_attn_ex", "rotatek_select_topr", "rotatek_decode_attn_partial",
-                       "rotatek_merge_partials"):
+                       "rotatek_merge_partials", "rotatek_decode_attn_ex2", "rotatek_compress_kv_ex2",
+                       "rotatek_calib_accumulate", "rotatek_calibrate_from_state"):
                 getattr(L, fn).restype = ctypes.c_int
             L.rotatek_status_string.argtypes = [ctypes.c_int]
             L.rotatek_status_string.restype = ctypes.c_char_p
@@ -214,6 +221,64 @@ def calibrate_subspace(K: torch.Tensor, Qw: torch.Tensor | None, V0: torch.Tenso
     return out
 
 
+def state_doubles(d: int) -> int:
+    """Doubles per calibration-state entry (ROTATEK_STATE_DOUBLES)."""
+    return d * d + 2 * d + 2
+
+
+def calib_state(state_units: int, head_dim: int, device="cuda") -> torch.Tensor:
+    """A zeroed calibration-statistics state [state_units, ROTATEK_STATE_DOUBLES(d)] f64."""
+    return torch.zeros((state_units, state_doubles(head_dim)), dtype=torch.float64, device=device)
+
+
+def calib_accumulate(K: torch.Tensor, Qw: torch.Tensor | None, state: torch.Tensor,
+                     flags: int = DEFAULT_FLAGS, *, ws: torch.Tensor | None = None,
+                     stream=None) -> torch.Tensor:
+    """Add the Alg. 1 sums of K [U, N, d] (and Qw [U, G, W, d]) into state[u % state_units]
+    (NEXT-3 offline calibration; token-sharded calibration before an all-reduce)."""
+    U, N, d = K.shape
+    if Qw is None:
+        G, W = 1, 0
+    else:
+        G, W = Qw.shape[1], Qw.shape[2]
+    nS = state.shape[0]
+    assert state.shape == (nS, state_doubles(d)) and state.dtype == torch.float64
+    dims = make_dims(U, G, d, 1, N, 0, W, _dtype_code(K))
+    if ws is None:
+        ws = workspace(dims, OP_CALIBRATE, K.device)
+    _check(lib().rotatek_calib_accumulate(ctypes.byref(dims), flags, _ptr(K),
+                                          _ptr(Qw) if W > 0 else None, nS, _ptr(state), _ptr(ws),
+                                          ws.numel(), _stream(stream)))
+    return state
+
+
+def calibrate_from_state(state: torch.Tensor, rank: int, flags: int = DEFAULT_FLAGS,
+                         dtype=torch.bfloat16, *, want_full: bool = False,
+                         ws: torch.Tensor | None = None, stream=None) -> dict:
+    """Alg. 1 from an accumulated state -> dict like calibrate() ([state_units, ...]).
+    dtype: the cache dtype the rotation is for (bf16: fp32 Jacobi + fp64 refinement)."""
+    nS = state.shape[0]
+    d = int(round((-2 + (4 + 4 * (state.shape[1] - 2)) ** 0.5) / 2))
+    dims = make_dims(nS, 1, d, rank, 1, 0, 0, BF16 if dtype == torch.bfloat16 else F32)
+    dev = state.device
+    out = dict(
+        R=torch.empty((nS, d, rank), dtype=torch.float32, device=dev),
+        dmu=torch.empty((nS, d), dtype=torch.float32, device=dev),
+        eigvals=torch.empty((nS, d), dtype=torch.float32, device=dev),
+        mask=torch.empty((nS, (d + 31) // 32), dtype=torch.int32, device=dev),
+        idx=torch.empty((nS, rank), dtype=torch.int32, device=dev),
+        info=torch.empty((nS,), dtype=torch.int32, device=dev),
+    )
+    out["R_full"] = torch.empty((nS, d, d), dtype=torch.float32, device=dev) if want_full else None
+    if ws is None:
+        ws = workspace(dims, OP_CALIBRATE, dev)
+    _check(lib().rotatek_calibrate_from_state(
+        ctypes.byref(dims), flags, _ptr(state), _ptr(out["R"]), _ptr(out["dmu"]),
+        _ptr(out["eigvals"]), _ptr(out["mask"]), _ptr(out["idx"]), _ptr(out["R_full"]),
+        _ptr(out["info"]), _ptr(ws), ws.numel(), _stream(stream)))
+    return out
+
+
 # --------------------------------------------------------------------------- compress
 def compress_kv(K: torch.Tensor, R: torch.Tensor, out: torch.Tensor | None = None,
                 stream=None, flags: int = 0) -> torch.Tensor:
@@ -221,12 +286,13 @@ def compress_kv(K: torch.Tensor, R: torch.Tensor, out: torch.Tensor | None = Non
     flags: SIMT_ONLY selects the CUDA-core kernel instead of tcgen05."""
     U, N, d = K.shape
     r = R.shape[2]
-    assert R.shape == (U, d, r) and R.dtype == torch.float32
+    nR = R.shape[0]   # nR < U: shared (offline) rotation, unit u uses R[u % nR]
+    assert R.shape == (nR, d, r) and U % nR == 0 and R.dtype == torch.float32
     if out is None:
         out = torch.empty((U, N, r), dtype=K.dtype, device=K.device)
     dims = make_dims(U, 1, d, r, N, 0, 0, _dtype_code(K))
-    _check(lib().rotatek_compress_kv_ex(ctypes.byref(dims), _ptr(K), _ptr(R), _ptr(out),
-                                        int(flags), _stream(stream)))
+    _check(lib().rotatek_compress_kv_ex2(ctypes.byref(dims), nR if nR != U else 0, _ptr(K), _ptr(R),
+                                         _ptr(out), int(flags), _stream(stream)))
     return out
 
 
@@ -241,17 +307,18 @@ def decode_attn(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, R: torch
     U, G, d = q.shape
     N, r = K_comp.shape[1], K_comp.shape[2]
     M = 0 if K_text is None else K_text.shape[1]
-    assert V.shape == (U, N, d) and R.shape == (U, d, r)
+    nR = R.shape[0]   # nR < U: shared (offline) rotation, unit u uses R[u % nR], dmu[u % nR]
+    assert V.shape == (U, N, d) and R.shape == (nR, d, r) and U % nR == 0
     dims = make_dims(U, G, d, r, N, M, 0, _dtype_code(K_comp))
     if out is None:
         out = torch.empty((U, G, d), dtype=torch.float32, device=q.device)
     if ws is None:
         ws = workspace(dims, OP_DECODE, q.device)
-    _check(lib().rotatek_decode_attn_ex(ctypes.byref(dims), _ptr(q), _ptr(K_comp), _ptr(V),
-                                        _ptr(R), _ptr(dmu), _ptr(K_text) if M else None,
-                                        _ptr(V_text) if M else None, float(scale), _ptr(out),
-                                        _ptr(ws), ws.numel(), int(splits), int(kernel),
-                                        _stream(stream)))
+    _check(lib().rotatek_decode_attn_ex2(ctypes.byref(dims), nR if nR != U else 0, _ptr(q),
+                                         _ptr(K_comp), _ptr(V), _ptr(R), _ptr(dmu),
+                                         _ptr(K_text) if M else None, _ptr(V_text) if M else None,
+                                         float(scale), _ptr(out), _ptr(ws), ws.numel(), int(splits),
+                                         int(kernel), _stream(stream)))
     return out
 
 

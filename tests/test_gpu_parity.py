@@ -452,3 +452,77 @@ def test_decode_token_shards_merge(rk, name, dtype):
     out = rk.merge_partials(torch.stack(parts))
     torch.cuda.synchronize()
     assert max_rel_err(to_np64(out), ref) <= TOL[dtype]
+
+
+# ------------------------------------------------------------------ NEXT-3 / 8(e) calibration state
+def _proj_dist(Ra, Rb):
+    return float(np.linalg.norm(Ra @ Ra.T - Rb @ Rb.T))
+
+
+@pytest.mark.parametrize("simt", [False, True])
+def test_offline_rotation_pooled_over_samples(rk, simt):
+    """NEXT-3: per-kv-head rotation accumulated over B calibration samples
+    (rotatek_calib_accumulate, state_units = H) equals the rotation of the pooled tokens
+    (oracle calibrate on the whole unit; G-cal gates), then reused across a batch: shared-R
+    compress (G-cmp) and shared-R decode (G-dec) against the oracle with R[u % H]."""
+    import torch
+    H, B, n = 2, 3, 300
+    cfg = CONFIGS["llava_b1"].with_(h_kv=H, n_vis=B * n, n_text=0)
+    w = make_workload(cfg, dist="gap", mean=5.0)
+    Kf = w["K"].f64()                                    # [H, B n, d]
+    Qw = w["Qw"].f64()
+    ref = orc.calibrate(Kf, Qw, cfg.rank)
+    Kt = to_torch(w["K"])
+    Ks = torch.cat([Kt[:, b * n:(b + 1) * n] for b in range(B)], 0).contiguous()   # u = b H + h
+    Qt = to_torch(w["Qw"])
+    Qs = torch.cat([Qt] + [torch.zeros_like(Qt)] * (B - 1), 0).contiguous()
+    flags = rk.DEFAULT_FLAGS | (rk.SIMT_ONLY if simt else 0)
+    st = rk.calib_accumulate(Ks, Qs, rk.calib_state(H, 128), flags)
+    cal = rk.calibrate_from_state(st, cfg.rank)
+    torch.cuda.synchronize()
+    assert (cal["info"].cpu().numpy() == 0).all()
+    R = to_np64(cal["R"])
+    for h in range(H):
+        assert _proj_dist(R[h], ref["R"][h]) <= 1e-3
+        assert np.linalg.norm(R[h].T @ R[h] - np.eye(cfg.rank)) <= 1e-3
+    np.testing.assert_allclose(to_np64(cal["dmu"]), orc.dmu_from_R(R, ref["mu"]), atol=1e-4, rtol=1e-5)
+    # reuse across a batch of B samples: K~ of unit u = b H + h with R[h]
+    Kc = rk.compress_kv(Ks, cal["R"])
+    torch.cuda.synchronize()
+    Rb = np.stack([R[u % H] for u in range(B * H)])
+    Ksf = to_np64(Ks)
+    want = orc.quantize(orc.compress(Ksf, Rb), "bf16")
+    got = to_np64(Kc)
+    absdot = np.einsum("uni,uir->unr", np.abs(Ksf), np.abs(Rb))
+    assert np.all(np.abs(got - want) <= 2.0 ** -7 * np.abs(want) + 64 * 2.0 ** -24 * absdot)
+    dmu = to_np64(cal["dmu"])
+    dmub = np.stack([dmu[u % H] for u in range(B * H)])
+    q = torch.randn(B * H, 1, 128, device="cuda").bfloat16()
+    V = torch.randn(B * H, n, 128, device="cuda").bfloat16()
+    out = rk.decode_attn(q, Kc, V, cal["R"], cal["dmu"])
+    torch.cuda.synchronize()
+    refo = orc.decode(to_np64(q), got, to_np64(V), Rb, dmub)
+    assert max_rel_err(to_np64(out), refo) <= TOL["bf16"]
+
+
+def test_token_sharded_calibration_state(rk):
+    """SURVEY 8(e) for U < P: each rank accumulates the Alg. 1 sums of its token slice, the
+    states are summed (all-reduce), every rank solves the same eigenproblem: equals the
+    unsharded calibration (oracle, G-cal gates) and the GPU's own rotatek_calibrate."""
+    import torch
+    cfg = CONFIGS["qwen_b1_r32"].with_(h_kv=2, n_vis=900, n_text=0)
+    w = make_workload(cfg, dist="gap", mean=0.5)
+    K, Qw = to_torch(w["K"]), to_torch(w["Qw"])
+    ref = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
+    direct = rk.calibrate(K, Qw, cfg.rank)
+    states = []
+    for sl, qw, fl in ((slice(0, 333), Qw, rk.DEFAULT_FLAGS), (slice(333, 900), None, rk.CENTER)):
+        states.append(rk.calib_accumulate(K[:, sl].contiguous(), qw, rk.calib_state(cfg.units, 128), fl))
+    st = states[0] + states[1]                       # the all-reduce (sum) of the shards
+    cal = rk.calibrate_from_state(st, cfg.rank)
+    torch.cuda.synchronize()
+    R, Rd = to_np64(cal["R"]), to_np64(direct["R"])
+    for u in range(cfg.units):
+        assert _proj_dist(R[u], ref["R"][u]) <= 1e-3
+        assert _proj_dist(R[u], Rd[u]) <= 1e-3
+    np.testing.assert_allclose(to_np64(cal["dmu"]), to_np64(direct["dmu"]), atol=1e-4, rtol=1e-4)

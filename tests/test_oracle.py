@@ -404,3 +404,46 @@ def test_budget_matches_paper_tables():
         m = orc.budget(row["token"], row["channel"])
         assert round(m + 1e-12, 2) == row["printed"], row
     assert orc.budget(1.0, 1.0) == 1.0
+
+
+def _planted(rng, U, N, d, r, mean=0.5):
+    """Keys with a planted top-r subspace (gap >> 1) per unit."""
+    out = np.empty((U, N, d))
+    for u in range(U):
+        Qo = np.linalg.qr(rng.standard_normal((d, d)))[0]
+        s = np.concatenate([np.linspace(3, 1, r), np.full(d - r, 0.05)])
+        out[u] = (rng.standard_normal((N, d)) * s) @ Qo.T + mean
+    return out
+
+
+def test_calib_state_pools_samples_and_token_shards():
+    """NEXT-3 / token-sharded calibration: Alg. 1 from accumulated sums.
+    (1) one unit per entry reproduces calibrate() (one-pass S - n mu mu^T vs two-pass C);
+    (2) splitting a unit's tokens over samples b (entries u % H) or over shards (states
+        added) reproduces calibrate() on the whole unit -- the window pooled once (Q4)."""
+    rng = np.random.default_rng(31)
+    H, n, d, r, G, W = 2, 50, 16, 4, 2, 3
+    K = _planted(rng, H, 3 * n, d, r)
+    Qw = rng.standard_normal((H, G, W, d))
+    ref = orc.calibrate(K, Qw, r)
+    one = orc.calibrate_from_state(orc.calib_state(K, Qw, H), r)
+    for h in range(H):
+        P = one["R"][h] @ one["R"][h].T
+        Pr = ref["R"][h] @ ref["R"][h].T
+        assert np.linalg.norm(P - Pr) <= 1e-9
+        np.testing.assert_allclose(one["dmu"][h], ref["dmu"][h], atol=1e-9)
+        np.testing.assert_allclose(one["lam"][h].sum(), np.trace(ref["Cq"][h]), rtol=1e-10)
+    # samples: unit b*H + h holds tokens [b n, (b+1) n) of head h; the window only in b = 0
+    Ks = np.concatenate([K[:, b * n:(b + 1) * n] for b in range(3)], axis=0)
+    Qs = np.concatenate([Qw] + [np.zeros_like(Qw)] * 2, axis=0)
+    pooled = orc.calibrate_from_state(orc.calib_state(Ks, Qs, H), r)
+    # token shards: two states added (an all-reduce), window in shard 0 only
+    st = orc.calib_state(K[:, :70], Qw, H)
+    st = orc.calib_state(K[:, 70:], None, H, state=st)
+    shard = orc.calibrate_from_state(st, r)
+    for res in (pooled, shard):
+        for h in range(H):
+            P = res["R"][h] @ res["R"][h].T
+            Pr = ref["R"][h] @ ref["R"][h].T
+            assert np.linalg.norm(P - Pr) <= 1e-9
+            np.testing.assert_allclose(res["dmu"][h], ref["dmu"][h], atol=1e-9)
