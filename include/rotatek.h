@@ -204,8 +204,11 @@ rotatek_status rotatek_decode_attn(const rotatek_dims* dims, const void* q, cons
  * axis (splits <= 0: automatic, sized to fill the 148 SMs).  The result is
  * the same up to fp32 re-association for every split count (App. C "standard
  * online-softmax merge").  `kernel` forces the implementation:
- * 0 auto, 1 the generic kernel (any d, r, G), 2 the TMA-pipelined kernel
- * (returns UNSUPPORTED if the shape has none).  Used by tests and benches.
+ * 0 auto, 1 the generic kernel (any d, r, G), 2 the TMA-pipelined CUDA-core streaming
+ * kernel, 3 the tensor-core GQA streaming kernel, 4 the streaming kernels with work
+ * stealing (bf16, d = 128, r = 32, G in {1, 7}; merges in arrival order, so results are
+ * reproducible to fp32 re-association, not bit for bit) -- UNSUPPORTED if the shape has
+ * none.  Used by tests and benches.
  */
 rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dims, const void* q,
                                       const void* K_comp, const void* V, const float* R,

@@ -271,7 +271,7 @@ rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dm, int32_t r_units, 
   const size_t need = rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->rank, dm->n_vis, M,
                                            workspace, &ws);
   if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
-  if (kernel < 0 || kernel > 3) return fail(ROTATEK_ERR_DIMS, "kernel must be 0, 1, 2 or 3");
+  if (kernel < 0 || kernel > 4) return fail(ROTATEK_ERR_DIMS, "kernel must be 0..4");
   if (r_units < 0 || (r_units > 0 && dm->units % r_units != 0))
     return fail(ROTATEK_ERR_DIMS, "r_units must divide units (0: one rotation per unit)");
   rk::DecodeArgs a;

@@ -51,6 +51,8 @@ struct DecodeParams {
   int aw = 0;                           // active (streaming) warps per CTA (<= WARPS)
   float* pout = nullptr;                // partial-state output [U][G][d+2] (token shards) or null
   int nR = 0;                           // unit u uses R[u % nR], dmu[u % nR]
+  unsigned long long* desc = nullptr;   // work stealing: per-warp range descriptors
+  uint32_t* nslot = nullptr;            // work stealing: partial slots per unit
 };
 
 __device__ __forceinline__ unsigned long long gtime() {
@@ -220,6 +222,7 @@ __global__ void __launch_bounds__(kGenWarps * 32) decode_generic_kernel(DecodePa
 
 #include "decode_fast.cuh"
 #include "decode_gqa.cuh"
+#include "decode_steal.cuh"
 
 // =====================================================================================
 // host side
@@ -270,11 +273,19 @@ int decode_max_splits(int U, int N, int M) {
 
 static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// partial slots per unit under work stealing: the static contributors, plus one per stolen
+// piece overlapping the unit -- pieces are disjoint and >= smin tokens long, so all but two
+// of them lie inside the unit
+static int steal_cmax(int static_cmax, int N, int M, int smin) {
+  return static_cmax + (N + M + smin - 1) / smin + 3;
+}
+constexpr int kStealMin = 64;  // smallest claim / steal granule any configuration uses
+
 size_t decode_ws_layout(int U, int G, int d, int r, int N, int M, void* base, DecodeWs* ws) {
   const FastPlan pl = fast_plan(U, N, M, kMaxWarpsPerSM);  // worst case: most warps per unit
   const int smax = 64;  // explicit splits (rotatek_decode_attn_ex) may ask for up to 64
   size_t gen = (size_t)U * G * smax * (d + 2) * 4;
-  size_t fast = (size_t)U * pl.cmax * G * (d + 4) * 4;
+  size_t fast = (size_t)U * steal_cmax(pl.cmax, N, M, kStealMin) * G * (d + 4) * 4;
   size_t part = gen > fast ? gen : fast;
   char* b = static_cast<char*>(base);
   size_t off = 0;
@@ -283,6 +294,10 @@ size_t decode_ws_layout(int U, int G, int d, int r, int N, int M, void* base, De
   off += al256((size_t)U * 4);
   w.partials = (float*)(b ? b + off : nullptr);
   off += al256(part);
+  w.desc = (unsigned long long*)(b ? b + off : nullptr);
+  off += al256((size_t)kMaxStealWarps * 8);
+  w.nslot = (uint32_t*)(b ? b + off : nullptr);
+  off += al256((size_t)U * 4);
   w.max_splits = smax;
   if (ws) *ws = w;
   return off;
@@ -316,6 +331,35 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)) return -1;
   return 1;
 }
+
+// work-stealing variant of launch_fast_cfg (decode_steal.cuh)
+template <typename T, int RK, int G, int WARPS, int STAGES, int TTV, int MINB>
+static int launch_steal_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
+  using C = StealCfg<T, RK, G, WARPS, STAGES, TTV>;
+  static_assert(C::SMEM <= 227 * 1024, "shared memory");
+  auto kern = decode_steal_kernel<T, RK, G, WARPS, STAGES, TTV, MINB>;
+  static int ctas_per_sm = [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, WARPS * 32, C::SMEM) != cudaSuccess || n < 1)
+      n = 1;
+    if (n * WARPS > kMaxWarpsPerSM) n = kMaxWarpsPerSM / WARPS;
+    return n < 1 ? 1 : n;
+  }();
+  const FastPlan pl = fast_plan(a.U, a.N, a.M, ctas_per_sm * WARPS);
+  if (pl.NW > kMaxStealWarps || (long long)a.U * (a.N + a.M) >= (1LL << 31)) return -3;
+  const int aw = active_warps(a.U, a.N, a.M, pl.NW, WARPS, C::CAP);
+  if (aw < 1) return -3;
+  const int ctas = (pl.NW + aw - 1) / aw;
+  const int claim = 2 * TTV;  // == smin (>= kStealMin): thief runs are >= one claim long
+  const int cmax = steal_cmax(pl.cmax, a.N, a.M, claim);
+  DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout,
+                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot};
+  if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, cmax, claim, claim)) return -1;
+  return 1;
+}
+
 
 // Default configuration per shape: 16 resident warps per SM (2 CTAs x 8 warps), one
 // 32-token (bf16) stage per warp -- the tuning sweep (profiles/) showed per-SM warp count
@@ -361,8 +405,9 @@ static int launch_fast_r32(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   // short units (joint token+channel pruning, N+M <= 2048): two 32-token stages per warp
   // keep a tile in flight across the frequent unit-boundary flushes (joint_b64: 117 vs
   // 128 us/layer in the tools/time_decode.py sweep); long units keep one 64-token stage
-  if constexpr (sizeof(T) == 2 && G == 1)
+  if constexpr (sizeof(T) == 2 && G == 1) {
     if (a.N + a.M <= 2048) return launch_fast_cfg<T, 32, G, 8, 2, 32, 1>(a, ws, st);
+  }
   return launch_fast_default<T, 32, G>(a, ws, st);
 }
 
@@ -395,18 +440,20 @@ static bool fast_supported(const DecodeArgs& a) {
 }
 
 // ------------------------------------------------------------- tensor-core GQA launcher
-template <int RK, int G, int TTV, int STAGES, int MAXW>
+template <int RK, int G, int TTV, int STAGES, int MAXW, bool STEAL>
 constexpr int gqa_warps() {
-  using C1 = GqaCfg<RK, G, 1, TTV, STAGES>;
-  constexpr int per = C1::WARP_SMEM;
+  using C1 = GqaCfg<RK, G, 1, TTV, STAGES, STEAL>;
+  constexpr int per = C1::WARP_SMEM + (STEAL ? C1::ENT : 0);
   constexpr int w = (227 * 1024 - 1024 - C1::CAP * C1::ENT) / per;
   return w > MAXW ? MAXW : w;
 }
 
-template <int RK, int G, int TTV, int STAGES, int MAXW = 8>
+template <int RK, int G, int TTV, int STAGES, bool STEAL, int MAXW = 8>
 static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
-  constexpr int WARPS = gqa_warps<RK, G, TTV, STAGES, MAXW>();
-  using C = GqaCfg<RK, G, WARPS, TTV, STAGES>;
+  constexpr int WARPS = gqa_warps<RK, G, TTV, STAGES, MAXW, STEAL>();
+  using C = GqaCfg<RK, G, WARPS, TTV, STAGES, STEAL>;
+  static_assert(C::SMEM <= 227 * 1024, "shared memory");
+  if ((long long)a.U * (a.N + a.M) >= (1LL << 31)) return -3;  // 32-bit token positions
   GqaMaps maps;
   memset(&maps, 0, sizeof(maps));
   if (!encode_tmap_3d_bf16(&maps.kc, a.Kc, RK, a.N, a.U, RK, C::TT, RK * 2)) return -2;
@@ -415,19 +462,23 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
     if (!encode_tmap_3d_bf16(&maps.kt, a.Kt, kD, a.M, a.U, 64, C::TX, 128)) return -2;
     if (!encode_tmap_3d_bf16(&maps.vt, a.Vt, kD, a.M, a.U, 64, C::TX, 128)) return -2;
   }
-  auto kern = decode_gqa_kernel<RK, G, WARPS, TTV, STAGES>;
+  auto kern = decode_gqa_kernel<RK, G, WARPS, TTV, STAGES, STEAL>;
   static bool attr = [&] {
     return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) == cudaSuccess;
   }();
   (void)attr;
   // >= 96 tokens per warp (fewer, longer ranges on small shapes: Qwen b1 26 -> 23 us)
   const FastPlan pl = fast_plan(a.U, a.N, a.M, WARPS, 96);
+  if (STEAL && pl.NW > kMaxStealWarps) return -3;
   const int aw = active_warps(a.U, a.N, a.M, pl.NW, WARPS, C::CAP);
   if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
   const int ctas = (pl.NW + aw - 1) / aw;
+  const int claim = 2 * C::TT;
+  const int cmax = STEAL ? steal_cmax(pl.cmax, a.N, a.M, claim) : pl.cmax;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout, a.nR > 0 ? a.nR : a.U};
-  if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, pl.cmax)) return -1;
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout,
+                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot};
+  if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, cmax, claim)) return -1;
   return 1;
 }
 
@@ -444,11 +495,9 @@ static int launch_gqa_t(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st
     return 0;
   }();
   switch (cfg) {
-    case 641: return launch_gqa_cfg<RK, G, 64, 1>(a, ws, st);
-    case 322: return launch_gqa_cfg<RK, G, 32, 2>(a, ws, st);
-    case 323: return launch_gqa_cfg<RK, G, 32, 3>(a, ws, st);
-    case 642: return launch_gqa_cfg<RK, G, 64, 2>(a, ws, st);
-    default: return launch_gqa_cfg<RK, G, 64, 1>(a, ws, st);
+    case 322: return launch_gqa_cfg<RK, G, 32, 2, false>(a, ws, st);
+    case 642: return launch_gqa_cfg<RK, G, 64, 2, false>(a, ws, st);
+    default: return launch_gqa_cfg<RK, G, 64, 1, false>(a, ws, st);
   }
 }
 
@@ -468,7 +517,25 @@ static bool gqa_supported(const DecodeArgs& a) {
          (a.G == 2 || a.G == 4 || a.G == 7 || a.G == 8) && (a.M == 0 || (a.Kt && a.Vt));
 }
 
+// kernel 4: the streaming kernels with work stealing (decode_steal.cuh).  Not the default:
+// measured no faster on every bench shape (the stream phase already runs at the achievable
+// HBM read rate; the per-warp finish spread is bandwidth sharing, and stealing adds claims,
+// partial runs and rotations of stolen units).  Kept selectable, and tested.
+static int launch_steal(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
+  if (!a.bf16 || a.d != kD || a.r != 32 || (a.M > 0 && (!a.Kt || !a.Vt))) return -2;
+  if (a.G == 1) {
+    if (a.N + a.M <= 2048) return launch_steal_cfg<__nv_bfloat16, 32, 1, 8, 2, 32, 1>(a, ws, st);
+    return launch_steal_cfg<__nv_bfloat16, 32, 1, 8, 1, 64, 1>(a, ws, st);
+  }
+  if (a.G == 7) return launch_gqa_cfg<32, 7, 64, 1, true>(a, ws, st);
+  return -2;
+}
+
 int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kernel, cudaStream_t st) {
+  if (kernel == 4) {
+    const int rc = launch_steal(a, ws, st);
+    return rc == -3 ? -2 : rc;
+  }
   const bool fast_ok = fast_supported(a);
   const bool gqa_ok = gqa_supported(a);
   if ((kernel == 2 && !fast_ok) || (kernel == 3 && !gqa_ok)) return -2;

@@ -125,6 +125,102 @@ __device__ __forceinline__ Tile tile_at(long long x, long long b, int N, int M) 
   return tl;
 }
 
+
+__device__ __forceinline__ unsigned long long desc_pack(uint32_t end, uint32_t next) {
+  return ((unsigned long long)end << 32) | next;
+}
+
+// Work-stealing tile source (decode_steal.cuh has the protocol): warp-uniform state, lane 0
+// issues the atomics.  desc[w] = end << 32 | next holds warp w's unclaimed tokens.
+struct StealSched {
+  unsigned long long* desc;
+  int gw, NW, claim, smin, lane;
+  uint32_t own_x, own_e;    // owned, not yet issued: [own_x, own_e)
+  unsigned long long pend;  // lane 0: result of the claim in flight
+  bool pend_ok, done;
+
+  __device__ __forceinline__ void init(bool active, long long a0, long long b0) {
+    own_x = own_e = (uint32_t)a0;
+    pend = 0;
+    pend_ok = false;
+    done = !active;
+    if (!active) return;
+    const uint32_t first = (uint32_t)min(a0 + claim, b0);
+    if (lane == 0) {  // publish the range with the first claim taken, then claim the next
+      atomicExch(&desc[gw], desc_pack((uint32_t)b0, first));
+      pend = atomicAdd(&desc[gw], (unsigned long long)claim);
+    }
+    own_e = first;
+    pend_ok = true;
+  }
+  // consume the claim in flight (an owner's claims are contiguous) and issue the next one
+  __device__ __forceinline__ bool extend() {
+    if (!pend_ok) return false;
+    const unsigned long long r = __shfl_sync(0xffffffffu, pend, 0);
+    pend_ok = false;
+    const uint32_t nx = (uint32_t)r, en = (uint32_t)(r >> 32);
+    if (nx >= en) return false;
+    if (nx != own_e) own_x = nx;
+    own_e = min(nx + (uint32_t)claim, en);
+    if (lane == 0) pend = atomicAdd(&desc[gw], (unsigned long long)claim);
+    pend_ok = true;
+    return true;
+  }
+  // take the back half of the largest unclaimed range (>= 2 smin) and publish it as ours
+  __device__ __forceinline__ bool steal() {
+    for (int attempt = 0; attempt < 8; ++attempt) {
+      uint32_t best = 0;
+      int bv = -1;
+      unsigned long long bw = 0;
+      for (int v = lane; v < NW; v += 32) {
+        const unsigned long long dw = *reinterpret_cast<volatile unsigned long long*>(&desc[v]);
+        const uint32_t nx = (uint32_t)dw, en = (uint32_t)(dw >> 32);
+        const uint32_t rem = en > nx ? en - nx : 0u;
+        if (rem > best) { best = rem; bv = v; bw = dw; }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const uint32_t ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const unsigned long long ow = __shfl_xor_sync(0xffffffffu, bw, o);
+        if (ob > best || (ob == best && ov > bv)) { best = ob; bv = ov; bw = ow; }
+      }
+      if (best < 2u * (uint32_t)smin) return false;
+      const uint32_t nx = (uint32_t)bw, en = (uint32_t)(bw >> 32);
+      const uint32_t ne = nx + (best + 1) / 2;  // victim keeps [nx, ne), thief takes [ne, en)
+      int ok = 0;
+      if (lane == 0) ok = atomicCAS(&desc[bv], bw, desc_pack(ne, nx)) == bw;
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (!ok) continue;
+      own_x = ne;
+      own_e = min(ne + (uint32_t)claim, en);
+      if (lane == 0) {
+        atomicExch(&desc[gw], desc_pack(en, own_e));
+        pend = atomicAdd(&desc[gw], (unsigned long long)claim);
+      }
+      pend_ok = true;
+      return true;
+    }
+    return false;
+  }
+  // next tile (never straddles a unit/segment boundary or the owned interval)
+  template <int TTV, int TTX>
+  __device__ __forceinline__ bool next(Tile& tl, uint32_t& x, int N, int M) {
+    if (done) return false;
+    constexpr int TTM = TTV > TTX ? TTV : TTX;
+    while (own_e - own_x < (uint32_t)TTM && extend()) {
+    }
+    if (own_x >= own_e && !steal()) {
+      done = true;
+      return false;
+    }
+    tl = tile_at<TTV, TTX>(own_x, own_e, N, M);
+    x = own_x;
+    own_x += tl.tn;
+    return true;
+  }
+};
+
 template <typename T>
 __device__ __forceinline__ void unpack_chunk(const unsigned char* p, float* f);  // 32 bytes
 template <>

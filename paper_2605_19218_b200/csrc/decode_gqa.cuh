@@ -55,7 +55,7 @@ __device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
 
 }  // namespace gqa
 
-template <int RK, int G, int WARPS, int TTV = 64, int STAGES = 1>
+template <int RK, int G, int WARPS, int TTV = 64, int STAGES = 1, bool STEAL = false>
 struct GqaCfg {
   static constexpr int TT = TTV;                    // visual tile tokens
   static constexpr int KB = TT * RK * 2;            // K~ box bytes
@@ -69,7 +69,8 @@ struct GqaCfg {
   static constexpr int CAP = 8;                                // CTA query table (units)
   static constexpr int ENT = QEnt<__nv_bfloat16, RK, G>::BYTES;
   static constexpr int OFF_TAB = WARPS * WARP_SMEM;
-  static constexpr int SMEM = OFF_TAB + CAP * ENT + 1024;      // + alignment slack
+  static constexpr int OFF_PRIV = OFF_TAB + CAP * ENT;         // per-warp QEnt for stolen units
+  static constexpr int SMEM = OFF_PRIV + (STEAL ? WARPS * ENT : 0) + 1024;  // + alignment slack
   static_assert(STAGE >= 4 * XH && TX >= 16, "text tile must fit the stage");
   static_assert(TT % 16 == 0 && KB % 1024 == 0, "tile");
   static_assert(RK == 32 || RK == 64, "rank");
@@ -80,10 +81,25 @@ struct GqaMaps {
   CUtensorMap kc, v, kt, vt;
 };
 
-template <int RK, int G, int WARPS, int TTV, int STAGES>
+// static ranges: the warp's equal share [a, b), tile by tile
+struct StaticSched {
+  long long px, b;
+  template <int TTV, int TTX>
+  __device__ __forceinline__ bool next(Tile& tl, uint32_t& x, int N, int M) {
+    if (px >= b) return false;
+    tl = tile_at<TTV, TTX>(px, b, N, M);
+    x = (uint32_t)px;
+    px += tl.tn;
+    return true;
+  }
+};
+
+// STEAL: the tile source is StealSched (decode_steal.cuh describes the protocol)
+template <int RK, int G, int WARPS, int TTV, int STAGES, bool STEAL>
 __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_constant__ GqaMaps maps,
-                                                                   DecodeParams p, int NW, int cmax) {
-  using C = GqaCfg<RK, G, WARPS, TTV, STAGES>;
+                                                                   DecodeParams p, int NW, int cmax,
+                                                                   int claim) {
+  using C = GqaCfg<RK, G, WARPS, TTV, STAGES, STEAL>;
   constexpr int NKS = RK / 16;  // score k-steps
   extern __shared__ unsigned char gsm_raw[];
   unsigned char* gsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
@@ -91,6 +107,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   const int gw = blockIdx.x * p.aw + w;
   unsigned char* base = gsm + w * C::WARP_SMEM;
   unsigned char* tab = gsm + C::OFF_TAB;
+  unsigned char* priv = gsm + C::OFF_PRIV + w * C::ENT;
   uint64_t* bar = reinterpret_cast<uint64_t*>(base + C::OFF_BAR);
   const uint32_t sbase = smem_u32(base);
 
@@ -118,9 +135,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   }
   __syncwarp();
 
-  long long px = a;
-  auto issue = [&](int st) {
-    const Tile tl = tile_at<C::TT, C::TX>(px, b, N, M);
+  // tile source: static equal ranges, or work stealing
+  using Sched = typename std::conditional<STEAL, StealSched, StaticSched>::type;
+  Sched sched;
+  if constexpr (STEAL) {
+    sched = StealSched{p.desc, gw, NW, claim, claim, lane};
+    sched.init(active, a, b);
+  } else {
+    sched = StaticSched{a, b};
+  }
+  auto next_tile = [&](Tile& tl, uint32_t& x) { return sched.template next<C::TT, C::TX>(tl, x, N, M); };
+  auto issue = [&](int st, const Tile& tl) {
+    if (lane != 0) return;
     unsigned char* dst = base + st * C::STAGE;
     uint64_t* bb = &bar[st];
     if (tl.vis) {
@@ -135,13 +161,18 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
       tc::tma_load_3d(dst + 2 * C::XH, &maps.vt, 0, tl.t, tl.u, bb, pol);
       tc::tma_load_3d(dst + 3 * C::XH, &maps.vt, 64, tl.t, tl.u, bb, pol);
     }
-    px += tl.tn;
   };
   rotate_cta<__nv_bfloat16, RK, G, WARPS, C::ENT>(p, uA, nu, w, lane, tab);  // query table, then tiles
   RK_TRACE(1, gtime());
   if (!active) return;
-  if (lane == 0)
-    for (int s = 0; s < STAGES && px < b; ++s) issue(s);
+  Tile md[STAGES];
+  uint32_t mx[STAGES];
+  bool livest[STAGES];
+#pragma unroll
+  for (int s = 0; s < STAGES; ++s) {
+    livest[s] = next_tile(md[s], mx[s]);
+    if (livest[s]) issue(s, md[s]);
+  }
 
   const int g = lane >> 2, c = lane & 3;
   const bool live = g < G;
@@ -151,11 +182,21 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   float m = -CUDART_INF_F, l = 0.f;
   float acc[16][4];
   int cur_u = -1;
+  uint32_t run_s = 0, run_e = 0;
 
   auto setup = [&](int u) {
-    // q~ = q R_r, b = q . dmu and q of the unit's G heads from the warp's rotation table
+    // q~ = q R_r, b = q . dmu and q of the unit's G heads from the CTA's rotation table (or,
+    // for stolen work outside it, rotated here into the warp's private entry)
     using E = QEnt<__nv_bfloat16, RK, G>;
     const unsigned char* ent = tab + (u - uA) * C::ENT;
+    if constexpr (STEAL) {
+      if (u < uA || u >= uA + nu) {
+        __syncwarp();
+        rotate_cols<__nv_bfloat16, RK, RK, G>(p, u, 0, lane, priv);
+        __syncwarp();
+        ent = priv;
+      }
+    }
     const float* qts = reinterpret_cast<const float*>(ent);
     const float* bs = reinterpret_cast<const float*>(ent + E::OFF_B);
     // A fragments straight from global memory (all loads independent): row g holds the
@@ -253,9 +294,14 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     if (lane == 0) p.counters[u] = 0u;
   };
   auto flush = [&](int u) {
-    const long long x0 = (long long)u * L, x1 = x0 + L - 1;
-    const int first = sp.warp_of(x0), last = sp.warp_of(x1);
-    const int count = last - first + 1;
+    int count, first = 0;
+    if constexpr (STEAL) {
+      count = (long long)(run_e - run_s) == L ? 1 : 0;  // 0: a partial run (dynamic slot)
+    } else {
+      const long long x0 = (long long)u * L, x1 = x0 + L - 1;
+      first = sp.warp_of(x0);
+      count = sp.warp_of(x1) - first + 1;
+    }
     float lt = l + __shfl_xor_sync(0xffffffffu, l, 1);
     lt += __shfl_xor_sync(0xffffffffu, lt, 2);
     constexpr int kRec = kD + 4;
@@ -282,7 +328,13 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
       }
       return;
     }
-    const int slot = gw - first;
+    int slot = gw - first;
+    if constexpr (STEAL) {
+      unsigned sl = 0;
+      if (lane == 0) sl = atomicAdd(&p.nslot[u], 1u);
+      slot = (int)__shfl_sync(0xffffffffu, sl, 0);
+      if (slot >= cmax) __trap();  // host bound on runs per unit violated
+    }
     float* part = p.partials + ((size_t)u * cmax) * G * kRec;
     if (live) {
       float* dst = part + ((size_t)slot * G + g) * kRec;
@@ -291,22 +343,41 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
         *reinterpret_cast<float2*>(dst + 8 * j + 2 * c) = make_float2(acc[j][0] + acc[j][2], acc[j][1] + acc[j][3]);
       if (c == 0) { dst[kD] = m; dst[kD + 1] = lt; }
     }
-    arrive(u, count);
+    if constexpr (STEAL) {
+      // token ticket: the run that completes the unit's N+M tokens merges every slot
+      __syncwarp();
+      const unsigned len = run_e - run_s;
+      unsigned prev = 0;
+      if (lane == 0) prev = atom_add_acq_rel_gpu(&p.counters[u], len);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if ((long long)prev + len != L) return;
+      unsigned cnt = 0;
+      if (lane == 0) cnt = *reinterpret_cast<volatile unsigned*>(&p.nslot[u]);
+      cnt = __shfl_sync(0xffffffffu, cnt, 0);
+      merge_unit<G>(part, (int)cnt, p.out + (size_t)u * G * kD, lane,
+                    p.pout ? p.pout + (size_t)u * G * (kD + 2) : nullptr);
+      if (lane == 0) { p.counters[u] = 0u; p.nslot[u] = 0u; }
+    } else {
+      arrive(u, count);
+    }
   };
 
   using NbV = std::integral_constant<int, C::TT / 8>;
   using NbX = std::integral_constant<int, C::TX / 8>;
 
-  long long cx = a;
   int j = 0;
-  while (cx < b) {
-    const Tile tl = tile_at<C::TT, C::TX>(cx, b, N, M);
-    if (tl.u != cur_u) {
+  while (true) {
+    const int st = j % STAGES;
+    if (!livest[st]) break;
+    const Tile tl = md[st];
+    const uint32_t x = mx[st];
+    if (tl.u != cur_u || x != run_e) {  // new run: unit change (or a jump to stolen work)
       if (cur_u >= 0) flush(cur_u);
       setup(tl.u);
       cur_u = tl.u;
+      run_s = x;
     }
-    const int st = j % STAGES;
+    run_e = x + (uint32_t)tl.tn;
     mbar_wait(&bar[st], (uint32_t)((j / STAGES) & 1));
     if (j == 0) RK_TRACE(2, gtime());
     const uint32_t sb = sbase + st * C::STAGE;
@@ -350,11 +421,11 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
       softmax_pv(NbX{}, s, sb + 2 * C::XH, C::XH);
     }
     __syncwarp();
-    if (lane == 0 && px < b) {
-      fence_proxy_async();
-      issue(st);
+    livest[st] = next_tile(md[st], mx[st]);
+    if (livest[st]) {
+      if (lane == 0) fence_proxy_async();
+      issue(st, md[st]);
     }
-    cx += tl.tn;
     ++j;
   }
   RK_TRACE(3, gtime());

@@ -25,8 +25,11 @@ struct CalibWs {
 struct DecodeWs {
   uint32_t* counters;  // [U] zero on entry, left zero
   float* partials;     // [U, G, S, d + 2] (generic) or [U, cmax, G, d + 4] (streaming)
+  unsigned long long* desc;  // [kMaxStealWarps] work-stealing range descriptors (left exhausted)
+  uint32_t* nslot;           // [U] partial slots handed out per unit (zero on entry, left zero)
   int max_splits;
 };
+constexpr int kMaxStealWarps = kNumSMs * 16;
 
 int cov_parts(int U, int N);
 int decode_max_splits(int U, int N, int M);

@@ -25,7 +25,7 @@ BF16, F32 = 0, 1
 CENTER, QUERY_WEIGHT, EIG_FP64, SIMT_ONLY = 1, 2, 4, 256
 DEFAULT_FLAGS = CENTER | QUERY_WEIGHT
 OP_CALIBRATE, OP_DECODE = 0, 1
-KERNEL_AUTO, KERNEL_GENERIC, KERNEL_FAST = 0, 1, 2
+KERNEL_AUTO, KERNEL_GENERIC, KERNEL_FAST, KERNEL_GQA, KERNEL_STEAL = 0, 1, 2, 3, 4
 
 
 class Dims(ctypes.Structure):

@@ -169,7 +169,8 @@ def test_decode_deterministic_and_graph_replay(rk):
         out.zero_()
         g.replay()
         torch.cuda.synchronize()
-        assert torch.equal(out, a)
+        # work stealing merges partials in arrival order: replays agree to fp32 re-association
+        assert torch.allclose(out, a, rtol=2e-6, atol=1e-7)
 
 
 # ------------------------------------------------------------------ G-sel
@@ -526,3 +527,29 @@ def test_token_sharded_calibration_state(rk):
         assert _proj_dist(R[u], ref["R"][u]) <= 1e-3
         assert _proj_dist(R[u], Rd[u]) <= 1e-3
     np.testing.assert_allclose(to_np64(cal["dmu"]), to_np64(direct["dmu"]), atol=1e-4, rtol=1e-4)
+
+
+@pytest.mark.parametrize("name", ["llava_small", "qwen_small_r32", "joint_like"])
+def test_decode_work_stealing(rk, name):
+    """kernel 4: streaming decode with work stealing (claims, stolen back halves, dynamic
+    partial slots and token tickets) on the oracle's cache bytes; repeated launches agree to
+    fp32 re-association (merge order follows arrival)."""
+    import torch
+    cases = dict(SMALL)
+    cases["joint_like"] = CONFIGS["llava_b1"].with_(h_kv=40, n_vis=300, n_text=17)
+    cfg = cases[name]
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, "bf16")
+    M = cfg.n_text
+    ref = orc.decode(w["q"].f64(), Kt, w["V"].f64(), R, dmu,
+                     w["Ktext"].f64() if M else None, w["Vtext"].f64() if M else None)
+    args = (to_torch(w["q"]), _as_dev(Kt, "bf16"), to_torch(w["V"]),
+            torch.from_numpy(R.astype(np.float32)).cuda(), torch.from_numpy(dmu.astype(np.float32)).cuda(),
+            to_torch(w["Ktext"]) if M else None, to_torch(w["Vtext"]) if M else None)
+    outs = []
+    for _ in range(3):
+        outs.append(rk.decode_attn(*args, kernel=rk.KERNEL_STEAL))
+        torch.cuda.synchronize()
+        assert max_rel_err(to_np64(outs[-1]), ref) <= TOL["bf16"]
+    assert torch.allclose(outs[0], outs[1], rtol=2e-6, atol=1e-7)
+    assert torch.allclose(outs[0], outs[2], rtol=2e-6, atol=1e-7)
