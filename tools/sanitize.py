@@ -17,8 +17,20 @@ for cfg in (CONFIGS["llava_b1"].with_(h_kv=2, n_vis=300, n_text=20),
     cal = rk.calibrate(K, dev(w["Qw"]), cfg.rank)
     sub = rk.calibrate_subspace(K, dev(w["Qw"]), torch.from_numpy(draw_v0(cfg)).cuda())
     Kc = rk.compress_kv(K, cal["R"])
-    for kern in (0, 1):
-        out = rk.decode_attn(dev(w["q"]), Kc, dev(w["V"]), cal["R"], cal["dmu"], dev(w["Ktext"]),
-                             dev(w["Vtext"]), kernel=kern)
+    args = (dev(w["q"]), Kc, dev(w["V"]), cal["R"], cal["dmu"], dev(w["Ktext"]), dev(w["Vtext"]))
+    for kern in (0, 1, 4):
+        if kern == 4 and cfg.head_dim != 128:
+            continue
+        out = rk.decode_attn(*args, kernel=kern)
+    # token shards (partial states + merge), offline state + shared rotation
+    half = cfg.n_vis // 2
+    parts = torch.stack([rk.decode_attn_partial(args[0], Kc[:, :half].contiguous(), args[2][:, :half].contiguous(),
+                                                cal["R"], cal["dmu"]),
+                         rk.decode_attn_partial(args[0], Kc[:, half:].contiguous(), args[2][:, half:].contiguous(),
+                                                cal["R"], cal["dmu"], args[5], args[6])])
+    rk.merge_partials(parts)
+    st = rk.calib_accumulate(K, dev(w["Qw"]), rk.calib_state(cfg.h_kv, cfg.head_dim))
+    off = rk.calibrate_from_state(st, cfg.rank)
+    rk.compress_kv(K, off["R"])
     torch.cuda.synchronize()
     print(cfg.name, "ok", float(out.abs().max()))
