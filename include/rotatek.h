@@ -209,7 +209,15 @@ rotatek_status rotatek_decode_attn(const rotatek_dims* dims, const void* q, cons
  * stealing (bf16, d = 128, r = 32, G in {1, 7}; merges in arrival order, so results are
  * reproducible to fp32 re-association, not bit for bit) -- UNSUPPORTED if the shape has
  * none.  Used by tests and benches.
+ * OR ROTATEK_DECODE_OVERLAP into `kernel` to launch the streaming kernels as programmatic
+ * dependents of the preceding work on `stream` (griddepcontrol): they start streaming the
+ * cache while that work finishes and wait for it only before reading q and the workspace.
+ * Contract: every input except q (K_comp, V, K_text, V_text, R, dmu) is complete before
+ * the PRECEDING kernel starts; q may be produced by it.  (Every streaming decode lets the
+ * next kernel launch early; a next kernel launched as a programmatic dependent must
+ * griddepcontrol.wait before reading out, as CUDA requires.)
  */
+#define ROTATEK_DECODE_OVERLAP 0x100
 rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dims, const void* q,
                                       const void* K_comp, const void* V, const float* R,
                                       const float* dmu, const void* K_text, const void* V_text,

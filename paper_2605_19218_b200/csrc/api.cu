@@ -271,7 +271,9 @@ rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dm, int32_t r_units, 
   const size_t need = rk::decode_ws_layout(dm->units, dm->group, dm->head_dim, dm->rank, dm->n_vis, M,
                                            workspace, &ws);
   if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
-  if (kernel < 0 || kernel > 4) return fail(ROTATEK_ERR_DIMS, "kernel must be 0..4");
+  const int overlap = (kernel & ROTATEK_DECODE_OVERLAP) ? 1 : 0;
+  kernel &= ~ROTATEK_DECODE_OVERLAP;
+  if (kernel < 0 || kernel > 4) return fail(ROTATEK_ERR_DIMS, "kernel must be 0..4 (| ROTATEK_DECODE_OVERLAP)");
   if (r_units < 0 || (r_units > 0 && dm->units % r_units != 0))
     return fail(ROTATEK_ERR_DIMS, "r_units must divide units (0: one rotation per unit)");
   rk::DecodeArgs a;
@@ -282,6 +284,7 @@ rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dm, int32_t r_units, 
   a.scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf((float)dm->head_dim);
   a.out = out;
   a.nR = r_units;
+  a.overlap = overlap;
   int n = 0;
   if ((s = launched(rk::launch_decode(a, ws, splits, kernel, reinterpret_cast<cudaStream_t>(stream)), &n)))
     return s;

@@ -53,7 +53,16 @@ struct DecodeParams {
   int nR = 0;                           // unit u uses R[u % nR], dmu[u % nR]
   unsigned long long* desc = nullptr;   // work stealing: per-warp range descriptors
   uint32_t* nslot = nullptr;            // work stealing: partial slots per unit
+  int overlap = 0;                      // programmatic dependent launch (ROTATEK_DECODE_OVERLAP)
 };
+
+// Programmatic dependent launch.  Every streaming decode lets the next kernel on the stream
+// launch early (it must then griddepcontrol.wait before reading out); with `overlap` the
+// decode itself was launched early and waits before its first read of q / workspace.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
@@ -309,6 +318,22 @@ static bool launch(Kern kern, int ctas, int threads, size_t smem, cudaStream_t s
   return cudaPeekAtLastError() == cudaSuccess;
 }
 
+// launch as a programmatic dependent of the preceding work on the stream
+template <typename Kern, typename... Args>
+static bool launch_overlap(Kern kern, int ctas, int threads, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ctas);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, args...) == cudaSuccess;
+}
+
 template <typename T, int RK, int G, int WARPS, int STAGES, int TTV, int MINB>
 static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
   using C = FastCfg<T, RK, G, WARPS, STAGES, TTV>;
@@ -327,8 +352,11 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
   const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
-                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout, a.nR > 0 ? a.nR : a.U};
-  if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)) return -1;
+                 a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout, a.nR > 0 ? a.nR : a.U,
+                 nullptr, nullptr, a.overlap};
+  if (!(a.overlap ? launch_overlap(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)
+                  : launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)))
+    return -1;
   return 1;
 }
 
@@ -477,8 +505,10 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
   const int cmax = STEAL ? steal_cmax(pl.cmax, a.N, a.M, claim) : pl.cmax;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout,
-                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot};
-  if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, cmax, claim)) return -1;
+                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot, a.overlap};
+  if (!(a.overlap ? launch_overlap(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, cmax, claim)
+                  : launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, cmax, claim)))
+    return -1;
   return 1;
 }
 

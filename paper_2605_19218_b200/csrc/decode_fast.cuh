@@ -451,6 +451,9 @@ template <typename T, int RK, int G, int WARPS, int ENT>
 __device__ __forceinline__ void rotate_cta(const DecodeParams& p, int uA, int nu, int w, int lane,
                                            unsigned char* tab) {
   constexpr int S = sizeof(T);
+  // ROTATEK_DECODE_OVERLAP: q (and the workspace) may still be in flight from the preceding
+  // kernel; every thread waits for it here (the first tile loads are already issued)
+  if (p.overlap) pdl_wait();
   int pu = 1;
   while (2 * pu * nu <= WARPS && 2 * pu <= 8) pu *= 2;
   // columns per item must keep >= one 16-byte q chunk of rows per lane: CW >= 4 * (16/S) / (kD/32)
@@ -637,10 +640,15 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
     }
     px += tl.tn;
   };
-  rotate_cta<T, RK, G, WARPS, C::ENT>(p, uA, nu, w, lane, tab);  // query table, then tiles
+  pdl_launch_dependents();
+  // query table, then tiles -- or, when launched overlapped with the preceding kernel, the
+  // first tiles (cache bytes are complete by contract) while it finishes, then the table
+  if (p.overlap && active && lane == 0)
+    for (int s = 0; s < STAGES && px < b; ++s) issue(s);
+  rotate_cta<T, RK, G, WARPS, C::ENT>(p, uA, nu, w, lane, tab);
   RK_TRACE(1, gtime());
   if (!active) return;
-  if (lane == 0)
+  if (!p.overlap && lane == 0)
     for (int s = 0; s < STAGES && px < b; ++s) issue(s);
 
   // ---------------- consumer state

@@ -162,17 +162,24 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
       tc::tma_load_3d(dst + 3 * C::XH, &maps.vt, 64, tl.t, tl.u, bb, pol);
     }
   };
-  rotate_cta<__nv_bfloat16, RK, G, WARPS, C::ENT>(p, uA, nu, w, lane, tab);  // query table, then tiles
-  RK_TRACE(1, gtime());
-  if (!active) return;
+  pdl_launch_dependents();
   Tile md[STAGES];
   uint32_t mx[STAGES];
   bool livest[STAGES];
+  auto first_tiles = [&] {
 #pragma unroll
-  for (int s = 0; s < STAGES; ++s) {
-    livest[s] = next_tile(md[s], mx[s]);
-    if (livest[s]) issue(s, md[s]);
-  }
+    for (int s = 0; s < STAGES; ++s) {
+      livest[s] = next_tile(md[s], mx[s]);
+      if (livest[s]) issue(s, md[s]);
+    }
+  };
+  // query table, then tiles -- or, when launched overlapped with the preceding kernel, the
+  // first tiles (cache bytes are complete by contract) while it finishes, then the table
+  if (p.overlap && active) first_tiles();
+  rotate_cta<__nv_bfloat16, RK, G, WARPS, C::ENT>(p, uA, nu, w, lane, tab);
+  RK_TRACE(1, gtime());
+  if (!active) return;
+  if (!p.overlap) first_tiles();
 
   const int g = lane >> 2, c = lane & 3;
   const bool live = g < G;

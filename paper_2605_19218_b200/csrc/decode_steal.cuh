@@ -82,6 +82,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_steal_kernel(DecodePa
     }
   };
 
+  pdl_launch_dependents();
   rotate_cta<T, RK, G, WARPS, C::ENT>(p, uA, nu, w, lane, tab);  // query table, then tiles
   RK_TRACE(1, gtime());
   if (!active) return;

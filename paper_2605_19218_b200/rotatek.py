@@ -26,6 +26,7 @@ CENTER, QUERY_WEIGHT, EIG_FP64, SIMT_ONLY = 1, 2, 4, 256
 DEFAULT_FLAGS = CENTER | QUERY_WEIGHT
 OP_CALIBRATE, OP_DECODE = 0, 1
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_FAST, KERNEL_GQA, KERNEL_STEAL = 0, 1, 2, 3, 4
+DECODE_OVERLAP = 0x100  # OR into kernel: programmatic dependent launch (include/rotatek.h)
 
 
 class Dims(ctypes.Structure):

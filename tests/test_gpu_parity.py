@@ -553,3 +553,44 @@ def test_decode_work_stealing(rk, name):
         assert max_rel_err(to_np64(outs[-1]), ref) <= TOL["bf16"]
     assert torch.allclose(outs[0], outs[1], rtol=2e-6, atol=1e-7)
     assert torch.allclose(outs[0], outs[2], rtol=2e-6, atol=1e-7)
+
+
+@pytest.mark.parametrize("name", ["llava_small", "qwen_small_r32"])
+def test_decode_overlap_reads_q_from_preceding_kernel(rk, name):
+    """ROTATEK_DECODE_OVERLAP: the decode is launched as a programmatic dependent of the
+    kernel that writes q (a torch op on the same stream) and of the previous decode (same
+    workspace, captured in a CUDA graph): it must wait for both before reading q /
+    the workspace.  Output equals the oracle on the final q (G-dec)."""
+    import torch
+    cfg = SMALL[name]
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, "bf16")
+    M = cfg.n_text
+    q0 = to_torch(w["q"])
+    cache = (_as_dev(Kt, "bf16"), to_torch(w["V"]), torch.from_numpy(R.astype(np.float32)).cuda(),
+             torch.from_numpy(dmu.astype(np.float32)).cuda(),
+             to_torch(w["Ktext"]) if M else None, to_torch(w["Vtext"]) if M else None)
+    qbuf = torch.empty_like(q0)
+    out1, out2 = torch.empty(q0.shape, device="cuda"), torch.empty(q0.shape, device="cuda")
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        ws = rk.workspace(rk.make_dims(cfg.units, cfg.group, 128, cfg.rank, cfg.n_vis, M, 0, rk.BF16),
+                          rk.OP_DECODE, "cuda")
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            qbuf.copy_(-q0)                      # decode 1 reads -q
+            rk.decode_attn(qbuf, *cache, out=out1, ws=ws, kernel=rk.DECODE_OVERLAP)
+            qbuf.copy_(q0)                       # written right before decode 2 (overlapped)
+            rk.decode_attn(qbuf, *cache, out=out2, ws=ws, kernel=rk.DECODE_OVERLAP)
+    for _ in range(3):
+        out1.zero_()
+        out2.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        ref = orc.decode(w["q"].f64(), Kt, w["V"].f64(), R, dmu,
+                         w["Ktext"].f64() if M else None, w["Vtext"].f64() if M else None)
+        refn = orc.decode(-w["q"].f64(), Kt, w["V"].f64(), R, dmu,
+                          w["Ktext"].f64() if M else None, w["Vtext"].f64() if M else None)
+        assert max_rel_err(to_np64(out2), ref) <= TOL["bf16"]
+        assert max_rel_err(to_np64(out1), refn) <= TOL["bf16"]
