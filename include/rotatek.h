@@ -299,6 +299,21 @@ rotatek_status rotatek_merge_partials(int32_t units, int32_t group, int32_t head
                                       rotatek_stream_t stream);
 
 /*
+ * Token pruning input (NEXT-2; FastV / VisionZip keep a scattered subset of the
+ * visual tokens, and calibration runs on the survivors only, Q20).  Compacts rows:
+ *   dst[u][j] = src[u][keep_idx[u][j]],  keep_idx [U, n_keep] int32 device (indices into
+ *   [0, n_src), any order; ascending keeps the original token order), src [U, n_src, ...],
+ *   dst [U, n_keep, ...] with row_bytes per token (d * sizeof(dtype): K, V, K~ ...).
+ * Apply to K (before rotatek_calibrate / rotatek_compress_kv) and V (for the decode).
+ * err (nullable) is set to 1 if an index is out of range (that row is zero-filled).
+ * Errors: DIMS (row_bytes must be a positive multiple of 16), NULL, ALIGN, CUDA.
+ */
+rotatek_status rotatek_gather_tokens(int32_t units, int32_t n_src, int32_t n_keep,
+                                     int32_t row_bytes, const int32_t* keep_idx,
+                                     const void* src, void* dst, int32_t* err,
+                                     rotatek_stream_t stream);
+
+/*
  * The top-r select + compaction step on its own (the selection half of
  * rotatek_calibrate, exposed so that it can be checked bit-exactly on given
  * eigenvalue arrays, including adversarial ties):

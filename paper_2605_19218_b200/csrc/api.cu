@@ -343,6 +343,23 @@ rotatek_status rotatek_decode_attn_partial(const rotatek_dims* dm, const void* q
   return ROTATEK_OK;
 }
 
+rotatek_status rotatek_gather_tokens(int32_t units, int32_t n_src, int32_t n_keep, int32_t row_bytes,
+                                     const int32_t* keep_idx, const void* src, void* dst, int32_t* err,
+                                     rotatek_stream_t stream) {
+  g_launches = 0;
+  if (units < 1 || n_src < 1 || n_keep < 1 || row_bytes < 16 || row_bytes % 16 != 0)
+    return fail(ROTATEK_ERR_DIMS, "bad gather dims (row_bytes: positive multiple of 16)");
+  if (!keep_idx || !src || !dst) return fail(ROTATEK_ERR_NULL, "keep_idx, src and dst are required");
+  if (!aligned16(src) || !aligned16(dst) || (reinterpret_cast<uintptr_t>(keep_idx) & 3u))
+    return fail(ROTATEK_ERR_ALIGN, "src/dst 16-byte, keep_idx 4-byte alignment");
+  int n = 0;
+  rotatek_status s = launched(rk::launch_gather_rows(units, n_src, n_keep, row_bytes, keep_idx, src, dst, err,
+                                                     reinterpret_cast<cudaStream_t>(stream)), &n);
+  if (s) return s;
+  g_launches = n;
+  return ROTATEK_OK;
+}
+
 rotatek_status rotatek_merge_partials(int32_t units, int32_t group, int32_t head_dim, int32_t nparts,
                                       const float* parts, float* out, rotatek_stream_t stream) {
   g_launches = 0;

@@ -62,4 +62,37 @@ int launch_compress(int U, int N, int d, int r, bool bf16, const void* K, const 
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
+// ============================================================== token gather (NEXT-2)
+// dst[u][j] = src[u][idx[u][j]] for row bytes `rb` (token pruning: FastV / VisionZip
+// keep a scattered subset of visual tokens; calibrate, compress and decode then run on the
+// compacted cache).  One warp per destination row, 16-byte vectors; out-of-range indices
+// set *err (the rows are zero-filled).
+__global__ void __launch_bounds__(256) gather_rows_kernel(int U, int n_src, int n_keep, int rb16,
+                                                          const int32_t* __restrict__ idx,
+                                                          const uint4* __restrict__ src,
+                                                          uint4* __restrict__ dst, int32_t* __restrict__ err) {
+  const long long row = (long long)blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= (long long)U * n_keep) return;
+  const int u = (int)(row / n_keep);
+  const int t = __ldg(idx + row);
+  uint4* d = dst + row * rb16;
+  if (t < 0 || t >= n_src) {
+    for (int e = lane; e < rb16; e += 32) d[e] = make_uint4(0u, 0u, 0u, 0u);
+    if (lane == 0 && err) atomicExch(err, 1);
+    return;
+  }
+  const uint4* s = src + ((long long)u * n_src + t) * rb16;
+  for (int e = lane; e < rb16; e += 32) d[e] = __ldcs(s + e);
+}
+
+int launch_gather_rows(int U, int n_src, int n_keep, int row_bytes, const int32_t* idx, const void* src,
+                       void* dst, int32_t* err, cudaStream_t st) {
+  const long long rows = (long long)U * n_keep;
+  gather_rows_kernel<<<(unsigned)((rows + 7) / 8), 256, 0, st>>>(U, n_src, n_keep, row_bytes / 16, idx,
+                                                                 static_cast<const uint4*>(src),
+                                                                 static_cast<uint4*>(dst), err);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
 }  // namespace rk

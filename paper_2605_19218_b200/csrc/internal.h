@@ -62,6 +62,8 @@ int launch_subspace(int U, int d, int k, int iters, double eps, bool center, con
                     const float* V0, float* R, float* dmu, float* ritz, int32_t* info, cudaStream_t st);
 int launch_select_only(int U, int d, int r, const float* lam, uint32_t* mask, int32_t* idx,
                        int32_t* info, cudaStream_t st);
+int launch_gather_rows(int U, int n_src, int n_keep, int row_bytes, const int32_t* idx, const void* src,
+                       void* dst, int32_t* err, cudaStream_t st);
 int launch_compress(int U, int N, int d, int r, bool bf16, const void* K, const float* R,
                     void* Kc, cudaStream_t st, int nR = 0);
 

@@ -78,11 +78,13 @@ def lib():
             L.rotatek_calibrate_from_state.argtypes = [dp, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                                        sz, vp]
             L.rotatek_merge_partials.argtypes = [i32, i32, i32, i32, vp, vp, vp]
+            L.rotatek_gather_tokens.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp]
             for fn in ("rotatek_calibrate", "rotatek_compress_kv", "rotatek_compress_kv_ex",
                        "rotatek_decode_attn",
                        "rotatek_decode_attn_ex", "rotatek_select_topr", "rotatek_decode_attn_partial",
                        "rotatek_merge_partials", "rotatek_decode_attn_ex2", "rotatek_compress_kv_ex2",
-                       "rotatek_calib_accumulate", "rotatek_calibrate_from_state"):
+                       "rotatek_calib_accumulate", "rotatek_calibrate_from_state",
+                       "rotatek_gather_tokens"):
                 getattr(L, fn).restype = ctypes.c_int
             L.rotatek_status_string.argtypes = [ctypes.c_int]
             L.rotatek_status_string.restype = ctypes.c_char_p
@@ -353,6 +355,20 @@ def merge_partials(parts: torch.Tensor, out: torch.Tensor | None = None, stream=
     if out is None:
         out = torch.empty((U, G, d), dtype=torch.float32, device=parts.device)
     _check(lib().rotatek_merge_partials(U, G, d, P, _ptr(parts), _ptr(out), _stream(stream)))
+    return out
+
+
+def gather_tokens(x: torch.Tensor, keep_idx: torch.Tensor, out: torch.Tensor | None = None,
+                  err: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Token pruning (NEXT-2): x [U, n_src, ...] -> [U, n_keep, ...] rows keep_idx [U, n_keep]."""
+    U, n_src = x.shape[0], x.shape[1]
+    n_keep = keep_idx.shape[1]
+    assert keep_idx.shape == (U, n_keep) and keep_idx.dtype == torch.int32
+    row_bytes = x[0, 0].numel() * x.element_size()
+    if out is None:
+        out = torch.empty((U, n_keep) + tuple(x.shape[2:]), dtype=x.dtype, device=x.device)
+    _check(lib().rotatek_gather_tokens(U, n_src, n_keep, row_bytes, _ptr(keep_idx), _ptr(x),
+                                       _ptr(out), _ptr(err), _stream(stream)))
     return out
 
 

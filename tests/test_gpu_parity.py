@@ -594,3 +594,38 @@ def test_decode_overlap_reads_q_from_preceding_kernel(rk, name):
                           w["Ktext"].f64() if M else None, w["Vtext"].f64() if M else None)
         assert max_rel_err(to_np64(out2), ref) <= TOL["bf16"]
         assert max_rel_err(to_np64(out1), refn) <= TOL["bf16"]
+
+
+def test_token_pruning_gather_end_to_end(rk):
+    """NEXT-2 / Q20: FastV-style scattered survivors.  rotatek_gather_tokens compacts K and
+    V bit-exactly; calibrate + compress + decode on the survivors match the oracle run on
+    the same surviving tokens (G-e2e); an out-of-range index raises the error flag."""
+    import torch
+    cfg = CONFIGS["llava_b1"].with_(h_kv=3, n_vis=400, n_text=16)
+    w = make_workload(cfg)
+    rng = np.random.default_rng(9)
+    keep = np.stack([np.sort(rng.choice(cfg.n_vis, 120, replace=False)) for _ in range(cfg.units)])
+    keep_t = torch.from_numpy(keep.astype(np.int32)).cuda()
+    K, V = to_torch(w["K"]), to_torch(w["V"])
+    Kk = rk.gather_tokens(K, keep_t)
+    Vk = rk.gather_tokens(V, keep_t)
+    torch.cuda.synchronize()
+    Kf, Vf = w["K"].f64(), w["V"].f64()
+    Ksel = np.take_along_axis(Kf, keep[:, :, None], axis=1)
+    Vsel = np.take_along_axis(Vf, keep[:, :, None], axis=1)
+    np.testing.assert_array_equal(to_np64(Kk), Ksel)
+    np.testing.assert_array_equal(to_np64(Vk), Vsel)
+    cal = rk.calibrate(Kk, to_torch(w["Qw"]), cfg.rank)
+    Kc = rk.compress_kv(Kk, cal["R"])
+    out = rk.decode_attn(to_torch(w["q"]), Kc, Vk, cal["R"], cal["dmu"], to_torch(w["Ktext"]),
+                         to_torch(w["Vtext"]))
+    torch.cuda.synchronize()
+    ref = orc.pipeline(Ksel, Vsel, w["Qw"].f64(), w["q"].f64(), cfg.rank, "bf16", w["Ktext"].f64(),
+                       w["Vtext"].f64())["out"]
+    assert max_rel_err(to_np64(out), ref) <= TOL["bf16"]
+    bad = keep_t.clone()
+    bad[1, 5] = cfg.n_vis
+    err = torch.zeros(1, dtype=torch.int32, device="cuda")
+    rk.gather_tokens(K, bad, err=err)
+    torch.cuda.synchronize()
+    assert int(err.item()) == 1
