@@ -7,9 +7,13 @@
 //   4-stage ring; one elected thread issues 8 tcgen05.mma (M=128, N=128, K=16) per chunk into
 //   one of two 128-column fp32 accumulators in TMEM; eight epilogue warps drain the other
 //   accumulator with tcgen05.ld and add it into fp64 registers, so each fp32 accumulation
-//   spans at most 128 tokens (exact bf16 products, fp32 per chunk, fp64 across chunks: the
-//   precision scheme of SURVEY Appendix A E-5/E-6).  The epilogue warps also form the column
-//   sums from the staged tile.  Out-of-range tokens of the last chunk are zero-filled by TMA.
+//   spans at most 256 tokens (exact bf16 products, fp32 per window, fp64 across windows: the
+//   precision scheme of SURVEY Appendix A E-5/E-6).  The column sums are a second MMA per
+//   16-token step, D_col[128 x 16] = K^T . ONES, into their own TMEM columns (no shared-memory
+//   pass: ring stages are released by the MMA commit alone).  PERSISTENT: one CTA per SM
+//   walks its (unit, part) items with running stage / window counters, so the next item's
+//   loads and MMAs overlap this item's epilogue.  Out-of-range tokens are zero-filled by TMA.
+//   llava_b32: 290 us -> 214 us (ncu), 3.9 TB/s.
 //
 // Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
 // warps 2..9 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4).
@@ -28,36 +32,44 @@ constexpr int kWin = 2;                  // chunks per fp32 TMEM accumulation wi
 constexpr int kHalfBytes = kTK * 128;    // one 64-channel half: kTK rows x 128 B
 constexpr int kStageBytes = 2 * kHalfBytes;
 constexpr int kThreads = 320;
-constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+constexpr int kOnesBytes = 2 * 16 * 128;  // all-ones B tile [16 rows][128 tokens], K-major SW128
+constexpr int kSmem = kStages * kStageBytes + kOnesBytes + 1024 + 256;
+constexpr int kTmemCols = 512;             // 2 x 128 Gram columns + 2 x 16 column-sum columns
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_constant__ CUtensorMap tmap, int N,
-                                                             int parts, double* __restrict__ covpart,
+                                                             int U, int parts, double* __restrict__ covpart,
                                                              double* __restrict__ colpart,
                                                              const double* __restrict__ sigma,
                                                              double* __restrict__ cq, double* __restrict__ mu,
                                                              bool center, bool fused) {
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
+  unsigned char* ones = sm + kStages * kStageBytes;  // 1024-aligned
+  uint64_t* full = reinterpret_cast<uint64_t*>(ones + kOnesBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
-  __shared__ double colred[16][kDc];
   __shared__ double colsum_sm[kDc];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.y, p = blockIdx.x;
+  // PERSISTENT: this CTA takes the work items (u, p) = blockIdx.x, + gridDim.x, ...; the ring
+  // stages and the two TMEM accumulators run continuously across items (running chunk and
+  // window counters), so the next item's loads and MMAs overlap this item's epilogue
   const int nchunks_all = (N + kTK - 1) / kTK;
-  const int c_lo = (int)((long long)nchunks_all * p / parts);
-  const int c_hi = (int)((long long)nchunks_all * (p + 1) / parts);
-  const int nch = c_hi - c_lo;
+  const int nitems = U * parts;
+  auto item_range = [&](int it, int& u, int& p, int& c_lo, int& nch) {
+    u = it / parts;
+    p = it % parts;
+    c_lo = (int)((long long)nchunks_all * p / parts);
+    nch = (int)((long long)nchunks_all * (p + 1) / parts) - c_lo;
+  };
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1 + 8);
+      mbar_init(&empty[s], 1);  // released by the MMA commit alone (no smem column-sum pass)
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -66,7 +78,12 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     fence_mbar_init();
     tc::prefetch_tmap(&tmap);
   }
-  if (warp == 1) tc::tmem_alloc(tmem_slot, 256);
+  // column sums on the tensor core too: D_col[128 x 16] = K^T . ONES (every column of D_col
+  // is sum_n K[n][i]); the all-ones tile's layout is immaterial (all elements equal)
+  for (int e = threadIdx.x; e < kOnesBytes / 16; e += blockDim.x)
+    reinterpret_cast<uint4*>(ones)[e] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  fence_proxy_async();  // generic-proxy writes must be visible to the tensor core (async proxy)
+  if (warp == 1) tc::tmem_alloc(tmem_slot, kTmemCols);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -75,35 +92,55 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
   if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
-      for (int i = 0; i < nch; ++i) {
-        const int s = i % kStages;
-        mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
-        unsigned char* dst = sm + s * kStageBytes;
-        mbar_arrive_expect_tx(&full[s], kStageBytes);
-        const int tok = (c_lo + i) * kTK;
-        tc::tma_load_3d(dst, &tmap, 0, tok, u, &full[s], pol);
-        tc::tma_load_3d(dst + kHalfBytes, &tmap, 64, tok, u, &full[s], pol);
+      int gi = 0;  // running chunk counter (ring stage / phase)
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int u, p, c_lo, nch;
+        item_range(it, u, p, c_lo, nch);
+        for (int i = 0; i < nch; ++i, ++gi) {
+          const int s = gi % kStages;
+          mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
+          unsigned char* dst = sm + s * kStageBytes;
+          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          const int tok = (c_lo + i) * kTK;
+          tc::tma_load_3d(dst, &tmap, 0, tok, u, &full[s], pol);
+          tc::tma_load_3d(dst + kHalfBytes, &tmap, 64, tok, u, &full[s], pol);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 128, true, true);
-      for (int i = 0; i < nch; ++i) {
-        // fp32 accumulation window = kWin chunks (kWin * 128 tokens <= 256, E-6)
-        const int s = i % kStages, wi = i / kWin, a = wi & 1;
-        const bool first = (i % kWin) == 0, last = (i % kWin) == kWin - 1 || i == nch - 1;
-        mbar_wait(&full[s], (i / kStages) & 1);
-        if (first) mbar_wait(&tempty[a], ((wi >> 1) & 1) ^ 1);
-        tc::fence_after();
-        const uint32_t base = smem_u32(sm + s * kStageBytes);
+      constexpr uint32_t idesc_col = tc::idesc_bf16_f32(128, 16, true, false);
+      const uint32_t obase = smem_u32(ones);
+      int gi = 0, gw = 0;  // running chunk / accumulation-window counters
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int u, p, c_lo, nch;
+        item_range(it, u, p, c_lo, nch);
+        (void)u; (void)p; (void)c_lo;
+        for (int i = 0; i < nch; ++i, ++gi) {
+          // fp32 accumulation window = kWin chunks (kWin * 128 tokens <= 256, E-6), never
+          // spanning two items
+          const int s = gi % kStages, a = gw & 1;
+          const bool first = (i % kWin) == 0, last = (i % kWin) == kWin - 1 || i == nch - 1;
+          mbar_wait(&full[s], (gi / kStages) & 1);
+          if (first) mbar_wait(&tempty[a], ((gw >> 1) & 1) ^ 1);
+          tc::fence_after();
+          const uint32_t base = smem_u32(sm + s * kStageBytes);
 #pragma unroll
-        for (int kk = 0; kk < kTK / 16; ++kk) {
-          // MN-major, SWIZZLE_128B: LBO = next 64-channel half, SBO = next 8-token group
-          const uint64_t desc = tc::smem_desc(base + kk * 16 * 128, kHalfBytes, 1024, tc::SWZ_128B);
-          tc::mma_bf16(tmem + a * 128, desc, desc, idesc, (first && kk == 0) ? 0u : 1u);
+          for (int kk = 0; kk < kTK / 16; ++kk) {
+            // MN-major, SWIZZLE_128B: LBO = next 64-channel half, SBO = next 8-token group
+            const uint64_t desc = tc::smem_desc(base + kk * 16 * 128, kHalfBytes, 1024, tc::SWZ_128B);
+            tc::mma_bf16(tmem + a * 128, desc, desc, idesc, (first && kk == 0) ? 0u : 1u);
+            const uint64_t od = tc::smem_desc(obase + (kk >> 2) * (kOnesBytes / 2) + (kk & 3) * 32, 16, 1024,
+                                              tc::SWZ_128B);
+            tc::mma_bf16(tmem + 256 + a * 16, desc, od, idesc_col, (first && kk == 0) ? 0u : 1u);
+          }
+          tc::commit(&empty[s]);
+          if (last) {
+            tc::commit(&tfull[a]);
+            ++gw;
+          }
         }
-        tc::commit(&empty[s]);
-        if (last) tc::commit(&tfull[a]);
       }
     }
   } else {
@@ -113,63 +150,43 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     const int h = e >> 2;          // accumulator column half
     const int row = 32 * q + lane;  // output row (channel i)
     const int et = e * 32 + lane;   // 0..255
-    const int c8 = et & 15;         // column sums: 8-channel chunk ...
-    const int rg = et >> 4;         // ... over token rows rg, rg + 16, ... of the chunk
+    int gi = 0, gw = 0;  // running chunk / window counters (as the producer and MMA warps)
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+    int u, p, c_lo, nch;
+    item_range(it, u, p, c_lo, nch);
+    (void)c_lo;
     double acc[64];
 #pragma unroll
     for (int j = 0; j < 64; ++j) acc[j] = 0.0;
-    double csum[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) csum[j] = 0.0;
-    for (int i = 0; i < nch; ++i) {
-      const int s = i % kStages, wi = i / kWin, a = wi & 1;
+    double csum = 0.0;  // column sum of channel `row` (warps of column half 0)
+    for (int i = 0; i < nch; ++i, ++gi) {
+      const int a = gw & 1, wph = (gw >> 1) & 1;
       const bool last = (i % kWin) == kWin - 1 || i == nch - 1;
-      // column sums from the staged (swizzled) tile: 16-byte loads, conflict-free
-      mbar_wait(&full[s], (i / kStages) & 1);
-      {
-        const unsigned char* half = sm + s * kStageBytes + (c8 >> 3) * kHalfBytes;
-        const int chunk = c8 & 7;
-        float fs[8];
-#pragma unroll
-        for (int j = 0; j < 8; ++j) fs[j] = 0.f;
-#pragma unroll
-        for (int k = 0; k < kTK / 16; ++k) {
-          const int n = rg + 16 * k;
-          const uint4 v = *reinterpret_cast<const uint4*>(half + n * 128 + ((chunk ^ (n & 7)) << 4));
-          fs[0] += bf16lo(v.x); fs[1] += bf16hi(v.x); fs[2] += bf16lo(v.y); fs[3] += bf16hi(v.y);
-          fs[4] += bf16lo(v.z); fs[5] += bf16hi(v.z); fs[6] += bf16lo(v.w); fs[7] += bf16hi(v.w);
-        }
-#pragma unroll
-        for (int j = 0; j < 8; ++j) csum[j] += (double)fs[j];
-      }
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&empty[s]);
       if (!last) continue;
       // drain the window's accumulator into fp64 (four loads in flight, one wait)
-      mbar_wait(&tfull[a], (wi >> 1) & 1);
+      mbar_wait(&tfull[a], wph);
+      ++gw;
       tc::fence_after();
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 128 + h * 64;
-      uint32_t r[4][16];
+      // two halves of 32 columns (fewer live registers next to the 64 fp64 accumulators)
+      uint32_t r[2][16], rc = 0;
+      if (h == 0) tc::ld_32x32b_x1(tmem + ((uint32_t)(32 * q) << 16) + 256 + a * 16, rc);
 #pragma unroll
-      for (int b = 0; b < 4; ++b) tc::ld_32x32b_x16(taddr + b * 16, r[b]);
-      tc::ld_wait();
+      for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+        for (int b = 0; b < 2; ++b) tc::ld_32x32b_x16(taddr + (2 * hh + b) * 16, r[b]);
+        tc::ld_wait();
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[(2 * hh + b) * 16 + j] += (double)__uint_as_float(r[b][j]);
+      }
+      if (h == 0) csum += (double)__uint_as_float(rc);
       tc::fence_before();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&tempty[a]);
-#pragma unroll
-      for (int b = 0; b < 4; ++b)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) acc[b * 16 + j] += (double)__uint_as_float(r[b][j]);
     }
-#pragma unroll
-    for (int j = 0; j < 8; ++j) colred[rg][8 * c8 + j] = csum[j];
-    // wait for all column sums (named barrier over the 8 epilogue warps)
-    asm volatile("bar.sync 1, 256;" ::: "memory");
-    if (et < kDc) {
-      double s = 0.0;
-      for (int k = 0; k < 16; ++k) s += colred[k][et];
-      colsum_sm[et] = s;
-    }
+    if (h == 0) colsum_sm[row] = csum;
     asm volatile("bar.sync 1, 256;" ::: "memory");
     if (fused) {
       // parts == 1: this CTA saw every token of the unit -> finalize here (mu, C, C_q)
@@ -194,11 +211,12 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
       if (et < kDc) colpart[((size_t)u * parts + p) * kDc + et] = colsum_sm[et];
     }
   }
+    }  // items
   tc::fence_before();
   __syncthreads();
   if (warp == 1) {
     tc::fence_after();
-    tc::tmem_dealloc(tmem, 256);
+    tc::tmem_dealloc(tmem, kTmemCols);
   }
 }
 
@@ -247,9 +265,11 @@ int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, c
     return cudaFuncSetAttribute(cov_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) == cudaSuccess;
   }();
   (void)attr;
-  dim3 grid(ws.parts, U);
+  // persistent: one CTA per SM over the U * parts work items (the ring runs across items)
+  const int nitems = U * ws.parts;
+  const int grid = nitems < kNumSMs ? nitems : kNumSMs;
   // parts == 1: the kernel also finalizes (mu, C = S - N mu mu^T, C_q) -- no finalize launch
-  cov_tc_kernel<<<grid, kThreads, kSmem, st>>>(map, N, ws.parts, ws.covpart, ws.colpart, ws.sigma, ws.cq,
+  cov_tc_kernel<<<grid, kThreads, kSmem, st>>>(map, N, U, ws.parts, ws.covpart, ws.colpart, ws.sigma, ws.cq,
                                                ws.mu, center, allow_fused && ws.parts == 1);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
