@@ -805,6 +805,171 @@ __global__ void __launch_bounds__(kRefThreads) refine_kernel(int d, const double
   for (int j = tid; j < d; j += blockDim.x) lam_out[(size_t)u * d + j] = (float)diag[j];
 }
 
+// Same refinement for d = 128 with every operand in shared memory: C (fp64, 128 KB) and V0
+// (fp32, 64 KB) are loaded once; T = C V0 is accumulated in registers and written over C
+// after a barrier; the Rayleigh quotients come from a diagonal pre-pass; per 4x4 tile B, G
+// and W are formed in registers, then W overwrites T; V = V0 + V0 W.  (refine_kernel
+// re-reads C and T from global / L2 in its inner loops: 1.86 ms for llava_b32 under ncu.)
+constexpr int kRefSmThreads = 256;
+__global__ void __launch_bounds__(kRefSmThreads, 1) refine_smem_kernel(const double* __restrict__ cq,
+                                                                       const float* __restrict__ v0g,
+                                                                       float* __restrict__ lam_out,
+                                                                       double* __restrict__ vout,
+                                                                       const int32_t* __restrict__ jinfo) {
+  constexpr int d = 128, nt = d / 4;
+  extern __shared__ __align__(16) unsigned char rsm_raw[];
+  double* Cs = reinterpret_cast<double*>(rsm_raw);            // [d][d] C, then T = C V0, then W
+  float* v0 = reinterpret_cast<float*>(Cs + d * d);           // [d][d]
+  __shared__ double diag[d];
+  const int u = blockIdx.x, tid = threadIdx.x;
+  if (jinfo[u] == -1) return;
+  const double* C = cq + (size_t)u * d * d;
+  for (int e = tid; e < d * d / 2; e += kRefSmThreads)
+    reinterpret_cast<double2*>(Cs)[e] = __ldg(reinterpret_cast<const double2*>(C) + e);
+  for (int e = tid; e < d * d / 4; e += kRefSmThreads)
+    reinterpret_cast<float4*>(v0)[e] = __ldg(reinterpret_cast<const float4*>(v0g + (size_t)u * d * d) + e);
+  __syncthreads();
+  // (1) T = C V0: thread t owns the 4x4 tiles t, t + 256, t + 512, t + 768
+  double acc[4][4][4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k)
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[k][a][b] = 0.0;
+#pragma unroll 1
+  for (int l = 0; l < d; ++l) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = tid + k * kRefSmThreads;
+      const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+      const float4 v4 = *reinterpret_cast<const float4*>(v0 + l * d + j0);
+      const double vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double c = Cs[(i0 + a) * d + l];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[k][a][b] = fma(c, vv[b], acc[k][a][b]);
+      }
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = tid + k * kRefSmThreads;
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) Cs[(i0 + a) * d + j0 + b] = acc[k][a][b];
+  }
+  __syncthreads();
+  // (2a) Rayleigh quotients lambda_i = B_ii / G_ii (B = V0^T T, G = V0^T V0)
+  if (tid < d) {
+    double bi = 0.0, gi = 0.0;
+    for (int l = 0; l < d; ++l) {
+      const double v = (double)v0[l * d + tid];
+      bi = fma(v, Cs[l * d + tid], bi);
+      gi = fma(v, v, gi);
+    }
+    diag[tid] = bi / gi;
+  }
+  __syncthreads();
+  double bmax = 0.0;
+  for (int i = 0; i < d; ++i) bmax = fmax(bmax, fabs(diag[i]));
+  // (2b)+(3) per 4x4 tile: B, G, then W_ij = (B_ij - lambda_j G_ij) / (lambda_j - lambda_i),
+  // W_jj = (1 - G_jj) / 2, kept in registers until every thread is done reading T
+  double W[4][4][4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = tid + k * kRefSmThreads;
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+    double Bv[4][4], Gv[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) Bv[a][b] = Gv[a][b] = 0.0;
+#pragma unroll 2
+    for (int l = 0; l < d; ++l) {
+      const float4 va = *reinterpret_cast<const float4*>(v0 + l * d + i0);
+      const float4 vb = *reinterpret_cast<const float4*>(v0 + l * d + j0);
+      const double2 t01 = *reinterpret_cast<const double2*>(Cs + l * d + j0);
+      const double2 t23 = *reinterpret_cast<const double2*>(Cs + l * d + j0 + 2);
+      const double xa[4] = {va.x, va.y, va.z, va.w}, xb[4] = {vb.x, vb.y, vb.z, vb.w};
+      const double tb[4] = {t01.x, t01.y, t23.x, t23.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          Bv[a][b] = fma(xa[a], tb[b], Bv[a][b]);
+          Gv[a][b] = fma(xa[a], xb[b], Gv[a][b]);
+        }
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const int i = i0 + a, j = j0 + b;
+        const double num = Bv[a][b] - diag[j] * Gv[a][b];
+        const double gap = diag[j] - diag[i];
+        double w;
+        if (i == j) w = 0.5 * (1.0 - Gv[a][b]);
+        else if (fabs(gap) > 1e-12 * bmax && fabs(num) < 0.1 * fabs(gap)) w = num / gap;
+        else w = 0.0;
+        W[k][a][b] = w;
+      }
+  }
+  __syncthreads();  // every thread is done reading T
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = tid + k * kRefSmThreads;
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) Cs[(i0 + a) * d + j0 + b] = W[k][a][b];
+  }
+  __syncthreads();
+  // (4) V = V0 + V0 W
+  double* Vo = vout + (size_t)u * d * d;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = tid + k * kRefSmThreads;
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[k][a][b] = (double)v0[(i0 + a) * d + j0 + b];
+  }
+#pragma unroll 1
+  for (int l = 0; l < d; ++l) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int t = tid + k * kRefSmThreads;
+      const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+      const double2 w01 = *reinterpret_cast<const double2*>(Cs + l * d + j0);
+      const double2 w23 = *reinterpret_cast<const double2*>(Cs + l * d + j0 + 2);
+      const double wv[4] = {w01.x, w01.y, w23.x, w23.y};
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        const double va = (double)v0[(i0 + a) * d + l];
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[k][a][b] = fma(va, wv[b], acc[k][a][b]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int t = tid + k * kRefSmThreads;
+    const int i0 = (t / nt) * 4, j0 = (t % nt) * 4;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+      *reinterpret_cast<double4*>(Vo + (size_t)(i0 + a) * d + j0) =
+          make_double4(acc[k][a][0], acc[k][a][1], acc[k][a][2], acc[k][a][3]);
+  }
+  for (int j = tid; j < d; j += kRefSmThreads) lam_out[(size_t)u * d + j] = (float)diag[j];
+}
+
 int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st) {
   if (fp64) {
     size_t sm = jacobi_smem_bytes(d, true);
@@ -826,6 +991,13 @@ int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st) {
     jacobi32_kernel<0><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return -1;
+  if (d == 128) {
+    const size_t rsm = (size_t)d * d * (8 + 4);
+    cudaFuncSetAttribute(refine_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
+    refine_smem_kernel<<<U, kRefSmThreads, rsm, st>>>(ws.cq, v32, ws.lam, static_cast<double*>(ws.vecs),
+                                                       ws.jinfo);
+    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
+  }
   const size_t rsm = (size_t)d * d * 4;
   cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
   refine_kernel<<<U, kRefThreads, rsm, st>>>(d, ws.cq, v32, ws.covpart, ws.lam,
