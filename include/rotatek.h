@@ -47,7 +47,7 @@
 extern "C" {
 #endif
 
-#define ROTATEK_ABI_VERSION 1
+#define ROTATEK_ABI_VERSION 2
 
 typedef struct CUstream_st* rotatek_stream_t; /* == cudaStream_t; NULL = legacy default */
 
@@ -90,6 +90,10 @@ typedef struct {
   int32_t n_text;       /* M >= 0 full-d prompt/text/generated tokens per unit          */
   int32_t q_window;     /* W >= 0 recent prefill queries per query head (paper: 32)     */
   rotatek_dtype dtype;  /* element type of K, V, Qw, q, K~, K_text, V_text              */
+  int32_t text_stride;  /* tokens per unit in the K_text / V_text ALLOCATIONS (>= n_text;
+                           0 => n_text, dense).  A capacity > n_text makes the full-d
+                           segment appendable in place during generation (NEXT-2, Q18):
+                           token m of unit u is at row u * text_stride + m.               */
 } rotatek_dims;
 
 /* Bytes of device workspace `op` needs for these dims (0 if dims are invalid). */

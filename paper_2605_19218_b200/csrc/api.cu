@@ -30,6 +30,8 @@ rotatek_status check_dims(const rotatek_dims* dm) {
   if (dm->n_text < 0) return fail(ROTATEK_ERR_DIMS, "n_text must be >= 0");
   if (dm->q_window < 0) return fail(ROTATEK_ERR_DIMS, "q_window must be >= 0");
   if (dm->dtype != ROTATEK_BF16 && dm->dtype != ROTATEK_F32) return fail(ROTATEK_ERR_DIMS, "bad dtype");
+  if (dm->text_stride < 0 || (dm->text_stride > 0 && dm->text_stride < dm->n_text))
+    return fail(ROTATEK_ERR_DIMS, "text_stride must be 0 or >= n_text");
   return ROTATEK_OK;
 }
 
@@ -281,6 +283,7 @@ rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dm, int32_t r_units, 
   a.bf16 = dm->dtype == ROTATEK_BF16;
   a.q = q; a.Kc = K_comp; a.V = V; a.R = R; a.dmu = dmu;
   a.Kt = M > 0 ? K_text : nullptr; a.Vt = M > 0 ? V_text : nullptr;
+  a.Ms = dm->text_stride > 0 ? dm->text_stride : M;
   a.scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf((float)dm->head_dim);
   a.out = out;
   a.nR = r_units;
@@ -334,6 +337,7 @@ rotatek_status rotatek_decode_attn_partial(const rotatek_dims* dm, const void* q
   a.bf16 = dm->dtype == ROTATEK_BF16;
   a.q = q; a.Kc = K_comp; a.V = V; a.R = R; a.dmu = dmu;
   a.Kt = M > 0 ? K_text : nullptr; a.Vt = M > 0 ? V_text : nullptr;
+  a.Ms = dm->text_stride > 0 ? dm->text_stride : M;
   a.scale = softmax_scale > 0.f ? softmax_scale : 1.0f / sqrtf((float)dm->head_dim);
   a.out = nullptr;
   a.pout = part;

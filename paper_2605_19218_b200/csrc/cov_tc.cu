@@ -239,10 +239,15 @@ static PFN_encode get_encode() {
 
 bool encode_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0,
                          uint32_t b1, int swizzle_bytes) {
+  return encode_tmap_3d_bf16_strided(map, base, d0, d1, d2, d1, b0, b1, swizzle_bytes);
+}
+
+bool encode_tmap_3d_bf16_strided(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                                 uint64_t d1_stride, uint32_t b0, uint32_t b1, int swizzle_bytes) {
   PFN_encode enc = get_encode();
   if (!enc) return false;
   cuuint64_t dims[3] = {d0, d1, d2};
-  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+  cuuint64_t strides[2] = {d0 * 2, d0 * d1_stride * 2};
   cuuint32_t box[3] = {b0, b1, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B

@@ -54,6 +54,7 @@ struct DecodeParams {
   unsigned long long* desc = nullptr;   // work stealing: per-warp range descriptors
   uint32_t* nslot = nullptr;            // work stealing: partial slots per unit
   int overlap = 0;                      // programmatic dependent launch (ROTATEK_DECODE_OVERLAP)
+  int Ms = 0;                           // K_text / V_text rows per unit (text_stride)
 };
 
 // Programmatic dependent launch.  Every streaming decode lets the next kernel on the stream
@@ -149,8 +150,8 @@ __global__ void __launch_bounds__(kGenWarps * 32) decode_generic_kernel(DecodePa
       kw = r;
     } else {
       const int t = m0 + idx - (n1 - n0);
-      krow = static_cast<const T*>(p.Kt) + ((size_t)u * p.M + t) * d;
-      vrow = static_cast<const T*>(p.Vt) + ((size_t)u * p.M + t) * d;
+      krow = static_cast<const T*>(p.Kt) + ((size_t)u * p.Ms + t) * d;
+      vrow = static_cast<const T*>(p.Vt) + ((size_t)u * p.Ms + t) * d;
       kw = d;
     }
     for (int g = 0; g < G; ++g) {
@@ -353,7 +354,7 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout, a.nR > 0 ? a.nR : a.U,
-                 nullptr, nullptr, a.overlap};
+                 nullptr, nullptr, a.overlap, a.Ms};
   if (!(a.overlap ? launch_overlap(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)
                   : launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)))
     return -1;
@@ -383,7 +384,7 @@ static int launch_steal_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_
   const int cmax = steal_cmax(pl.cmax, a.N, a.M, claim);
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout,
-                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot};
+                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot, 0, a.Ms};
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, cmax, claim, claim)) return -1;
   return 1;
 }
@@ -487,8 +488,8 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
   if (!encode_tmap_3d_bf16(&maps.kc, a.Kc, RK, a.N, a.U, RK, C::TT, RK * 2)) return -2;
   if (!encode_tmap_3d_bf16(&maps.v, a.V, kD, a.N, a.U, 64, C::TT, 128)) return -2;
   if (a.M > 0) {
-    if (!encode_tmap_3d_bf16(&maps.kt, a.Kt, kD, a.M, a.U, 64, C::TX, 128)) return -2;
-    if (!encode_tmap_3d_bf16(&maps.vt, a.Vt, kD, a.M, a.U, 64, C::TX, 128)) return -2;
+    if (!encode_tmap_3d_bf16_strided(&maps.kt, a.Kt, kD, a.M, a.U, a.Ms, 64, C::TX, 128)) return -2;
+    if (!encode_tmap_3d_bf16_strided(&maps.vt, a.Vt, kD, a.M, a.U, a.Ms, 64, C::TX, 128)) return -2;
   }
   auto kern = decode_gqa_kernel<RK, G, WARPS, TTV, STAGES, STEAL>;
   static bool attr = [&] {
@@ -505,7 +506,7 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
   const int cmax = STEAL ? steal_cmax(pl.cmax, a.N, a.M, claim) : pl.cmax;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout,
-                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot, a.overlap};
+                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot, a.overlap, a.Ms};
   if (!(a.overlap ? launch_overlap(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, cmax, claim)
                   : launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, cmax, claim)))
     return -1;
@@ -584,7 +585,7 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
   if (S > ws.max_splits) S = ws.max_splits;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, nullptr, 0, a.pout,
-                 a.nR > 0 ? a.nR : a.U};
+                 a.nR > 0 ? a.nR : a.U, nullptr, nullptr, 0, a.Ms};
   size_t sm = ((size_t)a.G * a.d + (size_t)a.G * a.r + a.G + 2 * kGenWarps * a.G +
                (size_t)kGenWarps * a.G * a.d) * sizeof(float);
   dim3 grid(S, a.U);

@@ -59,31 +59,15 @@ struct FastCfg {
   static_assert(STAGE % 16 == 0, "stage alignment");
 };
 
-// Warp gw's token range is [start(gw), start(gw + 1)).  With av, ax > 1 the
-// equal split is rounded to the unit's visual (av) / text (ax) tile grid, so that a tensor-
-// map box (always a full tile) never reads tokens of the neighbouring warp's range (the
-// GQA kernel re-read ~7% of its bytes at range ends without it, ncu).
+// Warp gw's token range is [start(gw), start(gw + 1)): an equal split of the flattened
+// token stream (every warp gets >= 1 token, the host guarantees >= 64).  Rounding the split
+// points to the tile grid (no tensor-map box over-read at range ends, ~7 % of the GQA bytes)
+// was measured no faster and is not done.
 struct Split {
   long long T, L;
-  int NW, N, av, ax;
-  __device__ __forceinline__ long long start(int gw) const {
-    const long long x = T * gw / NW;
-    if (av == 1 && ax == 1) return x;
-    const long long u = x / L;
-    const int off = (int)(x - u * L);
-    int o;
-    if (off < N) {
-      o = (off + av / 2) / av * av;
-      if (o > N) o = N;
-    } else {
-      const int M = (int)(L - N);
-      int ox = (off - N + ax / 2) / ax * ax;
-      if (ox > M) ox = M;
-      o = N + ox;
-    }
-    return u * L + o;
-  }
-  // warp whose (non-empty) range contains global token x
+  int NW, N;
+  __device__ __forceinline__ long long start(int gw) const { return T * gw / NW; }
+  // warp whose range contains global token x
   __device__ __forceinline__ int warp_of(long long x) const {
     int g = (int)(x * NW / T);
     if (g >= NW) g = NW - 1;
@@ -92,8 +76,6 @@ struct Split {
     return g;
   }
 };
-// No range is ever empty: the host gives every warp >= 1 token (unrounded) or >= 96 tokens
-// (rounded: rounding moves a split point by <= av/2, ax/2 <= 32 tokens).
 
 struct Tile {
   int u;      // unit
@@ -605,7 +587,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
   const long long Ttot = L * p.U;
   RK_TRACE(0, gtime());
   int uA, nu;
-  const Split sp{Ttot, L, NW, N, 1, 1};
+  const Split sp{Ttot, L, NW, N};
   cta_units(sp, p.aw, blockIdx.x, uA, nu);
   const long long a = sp.start(gw), b = sp.start(gw + 1);
   const bool active = w < p.aw && gw < NW && a < b;
@@ -635,8 +617,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_fast_kernel(DecodePar
     } else {
       const uint32_t kb = (uint32_t)tl.tn * kD * C::S;
       mbar_arrive_expect_tx(&bar[st], 2 * kb);
-      bulk_g2s(dst, Kt + ((size_t)tl.u * M + tl.t) * kD, kb, &bar[st], pol);
-      bulk_g2s(dst + C::TT_X * kD * C::S, Vt + ((size_t)tl.u * M + tl.t) * kD, kb, &bar[st], pol);
+      bulk_g2s(dst, Kt + ((size_t)tl.u * p.Ms + tl.t) * kD, kb, &bar[st], pol);
+      bulk_g2s(dst + C::TT_X * kD * C::S, Vt + ((size_t)tl.u * p.Ms + tl.t) * kD, kb, &bar[st], pol);
     }
     px += tl.tn;
   };

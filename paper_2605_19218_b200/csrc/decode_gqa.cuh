@@ -116,9 +116,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
   const long long Ttot = L * p.U;
   RK_TRACE(0, gtime());
   int uA, nu;
-  // equal split (rounding the split points to the tile grid removes the ~7% box over-read at
-  // range ends but measured no faster: Split av/ax = C::TT/C::TX)
-  const Split sp{Ttot, L, NW, N, 1, 1};
+  const Split sp{Ttot, L, NW, N};
   cta_units(sp, p.aw, blockIdx.x, uA, nu);
   const long long a = sp.start(gw), b = sp.start(gw + 1);
   const bool active = w < p.aw && gw < NW && a < b;

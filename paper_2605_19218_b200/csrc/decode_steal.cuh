@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_steal_kernel(DecodePa
   const long long Ttot = L * p.U;
   RK_TRACE(0, gtime());
   int uA, nu;
-  const Split sp{Ttot, L, NW, N, 1, 1};
+  const Split sp{Ttot, L, NW, N};
   cta_units(sp, p.aw, blockIdx.x, uA, nu);
   const long long a0 = sp.start(gw), b0 = sp.start(gw + 1);
   const bool active = w < p.aw && gw < NW && a0 < b0;
@@ -77,8 +77,8 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_steal_kernel(DecodePa
     } else {
       const uint32_t kb = (uint32_t)tl.tn * kD * C::S;
       mbar_arrive_expect_tx(&bar[st], 2 * kb);
-      bulk_g2s(dst, Kt + ((size_t)tl.u * M + tl.t) * kD, kb, &bar[st], pol);
-      bulk_g2s(dst + C::TT_X * kD * C::S, Vt + ((size_t)tl.u * M + tl.t) * kD, kb, &bar[st], pol);
+      bulk_g2s(dst, Kt + ((size_t)tl.u * p.Ms + tl.t) * kD, kb, &bar[st], pol);
+      bulk_g2s(dst + C::TT_X * kD * C::S, Vt + ((size_t)tl.u * p.Ms + tl.t) * kD, kb, &bar[st], pol);
     }
   };
 

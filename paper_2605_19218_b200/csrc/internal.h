@@ -82,6 +82,7 @@ struct DecodeArgs {
   float* pout = nullptr;  // token-shard partial state [U][G][d+2] instead of out
   int nR = 0;             // distinct rotations: unit u uses R[u % nR], dmu[u % nR] (0: nR = U)
   int overlap = 0;        // ROTATEK_DECODE_OVERLAP: programmatic dependent launch
+  int Ms = 0;             // K_text / V_text rows per unit (text_stride; >= M)
 };
 // kernel: 0 auto, 1 generic, 2 fast.  Returns launches, -1 launch error, -2 unsupported.
 int launch_merge_parts(int U, int G, int d, int P, const float* parts, float* out, cudaStream_t st);

@@ -100,5 +100,8 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
 // host: encode a 3-D bf16 tensor map [d2][d1][d0] (d0 innermost) with box {b0, b1, 1}
 bool encode_tmap_3d_bf16(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                          uint32_t b0, uint32_t b1, int swizzle_bytes);
+// same with an explicit dim-2 stride: rows of dim 1 per dim-2 index (>= d1)
+bool encode_tmap_3d_bf16_strided(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                                 uint64_t d1_stride, uint32_t b0, uint32_t b1, int swizzle_bytes);
 
 }  // namespace rk

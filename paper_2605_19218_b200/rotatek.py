@@ -33,7 +33,8 @@ class Dims(ctypes.Structure):
     _fields_ = [("units", ctypes.c_int32), ("group", ctypes.c_int32),
                 ("head_dim", ctypes.c_int32), ("rank", ctypes.c_int32),
                 ("n_vis", ctypes.c_int32), ("n_text", ctypes.c_int32),
-                ("q_window", ctypes.c_int32), ("dtype", ctypes.c_int32)]
+                ("q_window", ctypes.c_int32), ("dtype", ctypes.c_int32),
+                ("text_stride", ctypes.c_int32)]
 
 
 class RotateKError(RuntimeError):
@@ -137,9 +138,10 @@ def _stream(stream):
     return ctypes.c_void_p(s.cuda_stream)
 
 
-def make_dims(units, group, head_dim, rank, n_vis, n_text=0, q_window=0, dtype=BF16) -> Dims:
+def make_dims(units, group, head_dim, rank, n_vis, n_text=0, q_window=0, dtype=BF16,
+              text_stride=0) -> Dims:
     return Dims(int(units), int(group), int(head_dim), int(rank), int(n_vis), int(n_text),
-                int(q_window), int(dtype))
+                int(q_window), int(dtype), int(text_stride))
 
 
 def workspace_bytes(dims: Dims, op: int) -> int:
@@ -304,15 +306,18 @@ def decode_attn(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, R: torch
                 dmu: torch.Tensor | None, K_text: torch.Tensor | None = None,
                 V_text: torch.Tensor | None = None, scale: float = 0.0,
                 out: torch.Tensor | None = None, *, splits: int = 0, kernel: int = KERNEL_AUTO,
-                ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+                n_text: int | None = None, ws: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
     """Alg. 2 for all query heads: q [U, G, d], K_comp [U, N, r], V [U, N, d], R [U, d, r],
-    dmu [U, d] | None, K_text/V_text [U, M, d] | None -> out [U, G, d] f32."""
+    dmu [U, d] | None, K_text/V_text [U, M_cap, d] | None -> out [U, G, d] f32.
+    n_text: the M <= M_cap valid full-d tokens (default M_cap): an appendable segment."""
     U, G, d = q.shape
     N, r = K_comp.shape[1], K_comp.shape[2]
-    M = 0 if K_text is None else K_text.shape[1]
+    Mcap = 0 if K_text is None else K_text.shape[1]
+    M = Mcap if n_text is None else int(n_text)
     nR = R.shape[0]   # nR < U: shared (offline) rotation, unit u uses R[u % nR], dmu[u % nR]
     assert V.shape == (U, N, d) and R.shape == (nR, d, r) and U % nR == 0
-    dims = make_dims(U, G, d, r, N, M, 0, _dtype_code(K_comp))
+    dims = make_dims(U, G, d, r, N, M, 0, _dtype_code(K_comp), Mcap if M else 0)
     if out is None:
         out = torch.empty((U, G, d), dtype=torch.float32, device=q.device)
     if ws is None:

@@ -629,3 +629,33 @@ def test_token_pruning_gather_end_to_end(rk):
     rk.gather_tokens(K, bad, err=err)
     torch.cuda.synchronize()
     assert int(err.item()) == 1
+
+
+@pytest.mark.parametrize("name", ["llava_small", "qwen_small_r32", "odd_r"])
+def test_appendable_text_segment_multistep(rk, name):
+    """NEXT-2 / Q18: generation appends (k_t, v_t) to the full-d segment in place -- K_text /
+    V_text are allocated with capacity M_cap and each step decodes n_text = M + t valid rows
+    (rotatek_dims.text_stride = M_cap); the current token attends to itself.  Every step
+    matches the oracle on the first n_text rows; rows beyond them are garbage on purpose."""
+    import torch
+    cfg = SMALL[name].with_(n_text=9)
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, "bf16")
+    steps, M0 = 4, cfg.n_text - 4
+    Mcap = cfg.n_text + 3
+    d = cfg.head_dim
+    Kx, Vx = w["Ktext"].f64(), w["Vtext"].f64()
+    kbuf = torch.randn(cfg.units, Mcap, d, device="cuda").bfloat16() * 100.0   # garbage tail
+    vbuf = torch.randn(cfg.units, Mcap, d, device="cuda").bfloat16() * 100.0
+    kbuf[:, :M0] = _as_dev(Kx[:, :M0], "bf16")
+    vbuf[:, :M0] = _as_dev(Vx[:, :M0], "bf16")
+    args = (to_torch(w["q"]), _as_dev(Kt, "bf16"), to_torch(w["V"]),
+            torch.from_numpy(R.astype(np.float32)).cuda(), torch.from_numpy(dmu.astype(np.float32)).cuda())
+    for t in range(steps):
+        M = M0 + t + 1
+        kbuf[:, M - 1] = _as_dev(Kx[:, M - 1], "bf16")                # append the new token
+        vbuf[:, M - 1] = _as_dev(Vx[:, M - 1], "bf16")
+        out = rk.decode_attn(*args, kbuf, vbuf, n_text=M)
+        torch.cuda.synchronize()
+        ref = orc.decode(w["q"].f64(), Kt, w["V"].f64(), R, dmu, Kx[:, :M], Vx[:, :M])
+        assert max_rel_err(to_np64(out), ref) <= TOL["bf16"], (t, M)
