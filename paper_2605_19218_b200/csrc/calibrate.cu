@@ -595,6 +595,7 @@ __global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* 
   }
   fro2 = block_sum<float>(fro2, red);
 
+  const float skip_thr = tol * sqrtf(fro2) / (float)d;
   int sweep = 0, converged = 0;
   for (;; ++sweep) {
     float off2 = 0.f;
@@ -616,7 +617,9 @@ __global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* 
         }
         const float apq = A[pk(p, q)];
         float c = 1.f, s = 0.f, t = 0.f;
-        if (apq != 0.f) {
+        // threshold: a rotation of |a_pq| <= skip_thr cannot matter at the stopping tolerance
+        // (all below it => off(A) <= tol ||A||_F), so it is skipped (s == 0 marks identity)
+        if (fabsf(apq) > skip_thr) {
           const float app = A[rowoff[p] + p], aqq = A[rowoff[q] + q];
           const float tau = (aqq - app) / (2.f * apq);
           t = (tau >= 0.f ? 1.f : -1.f) / (fabsf(tau) + sqrtf(1.f + tau * tau));
@@ -634,16 +637,19 @@ __global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* 
         const int a = ab & 0xFFFF, b = ab >> 16;
         const uint32_t pqa = PQ[a];
         const int pa = pqa & 0xFFFF, qa = pqa >> 16;
+        const float2 ca2 = csn[a];
         if (a == b) {
+          if (ca2.y == 0.f) continue;  // identity rotation: nothing to do
           const int ipq = pk(pa, qa);
           const float apq = A[ipq], t = tt[a];
           A[rowoff[pa] + pa] -= t * apq;
           A[rowoff[qa] + qa] += t * apq;
           A[ipq] = 0.f;
         } else {
+          const float2 cb2 = csn[b];
+          if (ca2.y == 0.f && cb2.y == 0.f) continue;  // both identity
           const uint32_t pqb = PQ[b];
           const int pb = pqb & 0xFFFF, qb = pqb >> 16;
-          const float2 ca2 = csn[a], cb2 = csn[b];
           const float ca = ca2.x, sa = ca2.y, cb = cb2.x, sb = cb2.y;
           const int i00 = pk(pa, pb), i01 = pk(pa, qb), i10 = pk(qa, pb), i11 = pk(qa, qb);
           const float x00 = A[i00], x01 = A[i01], x10 = A[i10], x11 = A[i11];
@@ -664,6 +670,7 @@ __global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* 
           const uint32_t pqb = PQ[b];
           const int pb = pqb & 0xFFFF, qb = pqb >> 16;
           const float2 c2 = csn[b];
+          if (c2.y == 0.f) continue;  // identity rotation
 #pragma unroll
           for (int jx = 0; jx < d / 32; ++jx) {
             const int x = lane + 32 * jx;
