@@ -517,6 +517,9 @@ __global__ void __launch_bounds__(kJ32Threads, 1) jacobi32_kernel(int d_rt, cons
 // upper 2x2 blocks (pair a <= pair b) becomes J_a^T X J_b (every element of A read and
 // written once), and V <- V J, between two barriers.
 constexpr int kJPThreads = 512;
+// threshold Jacobi: during the first 3 sweeps rotations with |a_pq| below kJacobiKappa x the
+// RMS off-diagonal are skipped (llava_b32: 13.1 -> 11.7 ms; kappa 0.3..0.6 equal, 1.0 worse)
+constexpr float kJacobiKappa = 0.4f;
 
 size_t jacobi32p_smem_bytes(int d) {
   const int h = d / 2;
@@ -595,7 +598,8 @@ __global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* 
   }
   fro2 = block_sum<float>(fro2, red);
 
-  const float skip_thr = tol * sqrtf(fro2) / (float)d;
+  const float final_thr = tol * sqrtf(fro2) / (float)d;
+  const float kappa = kJacobiKappa;
   int sweep = 0, converged = 0;
   for (;; ++sweep) {
     float off2 = 0.f;
@@ -606,6 +610,10 @@ __global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* 
     off2 = block_sum<float>(off2, red);
     if (off2 <= tol * tol * fro2) { converged = 1; break; }
     if (sweep >= max_sweeps) break;
+    // threshold Jacobi: in the first sweeps only entries above kappa x the RMS off-diagonal
+    // are annihilated (the rest shrink anyway); later only the final threshold applies
+    const float skip_thr = sweep < 3 ? fmaxf(final_thr, kappa * sqrtf(off2 / (float)(d * (d - 1))))
+                                     : final_thr;
     for (int k = 0; k < d - 1; ++k) {
       if (tid < h) {
         // circle-method pairs (no p < q swap: the rotation is symmetric in p and q)
