@@ -1,7 +1,8 @@
-"""Diagnostics: per-stage GPU vs oracle errors for a config (prints, no asserts)."""
+"""Diagnostics (test infrastructure, not a test): per-stage GPU vs oracle errors for a
+config (prints, no asserts).  Lives under tests/ because only tests may use oracle/."""
 import sys, os
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests"))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))  # repo root
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))  # tests/
 import numpy as np, torch
 import paper_2605_19218_b200 as rk
 from oracle import oracle as orc
