@@ -527,9 +527,16 @@ static int launch_gqa_t(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st
   }();
   switch (cfg) {
     case 322: return launch_gqa_cfg<RK, G, 32, 2, false>(a, ws, st);
+    case 641: return launch_gqa_cfg<RK, G, 64, 1, false>(a, ws, st);
     case 642: return launch_gqa_cfg<RK, G, 64, 2, false>(a, ws, st);
-    default: return launch_gqa_cfg<RK, G, 64, 1, false>(a, ws, st);
+    default: break;
   }
+  // r = 32, >= 64 units of <= 16K tokens: two 64-token stages per warp (fewer warps, so fewer
+  // partials per unit, and each warp's next tile in flight during its compute): qwen b32
+  // 44.8 -> 43.6 us, U = 64 x 4K tokens 37.3 -> 31.8; long units (32K), few units (U = 32:
+  // 26.9 -> 28.9) and r = 64 keep one stage per warp and more warps (tools/time_decode.py)
+  if (RK == 32 && a.U >= 64 && a.N + a.M <= 16384) return launch_gqa_cfg<RK, G, 64, 2, false>(a, ws, st);
+  return launch_gqa_cfg<RK, G, 64, 1, false>(a, ws, st);
 }
 
 template <int RK>
