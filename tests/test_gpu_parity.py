@@ -659,3 +659,28 @@ def test_appendable_text_segment_multistep(rk, name):
         torch.cuda.synchronize()
         ref = orc.decode(w["q"].f64(), Kt, w["V"].f64(), R, dmu, Kx[:, :M], Vx[:, :M])
         assert max_rel_err(to_np64(out), ref) <= TOL["bf16"], (t, M)
+
+
+def test_debug_decode_trace_stamps(rk):
+    """Diagnostics hook: the streaming kernels stamp per-warp %globaltimer values in order
+    (start <= rotated <= first tile <= loop end <= end) and the tile count."""
+    import torch
+    cfg = SMALL["llava_small"]
+    w = make_workload(cfg)
+    R, dmu, Kt = _cache_from_oracle(cfg, w, "bf16")
+    buf = torch.zeros(148 * 16 * 8, dtype=torch.int64, device="cuda")
+    rk.debug_decode_trace(buf)
+    try:
+        rk.decode_attn(to_torch(w["q"]), _as_dev(Kt, "bf16"), to_torch(w["V"]),
+                       torch.from_numpy(R.astype(np.float32)).cuda(),
+                       torch.from_numpy(dmu.astype(np.float32)).cuda(), to_torch(w["Ktext"]),
+                       to_torch(w["Vtext"]))
+        torch.cuda.synchronize()
+    finally:
+        rk.debug_decode_trace(None)
+    t = buf.view(-1, 8).cpu().numpy()
+    t = t[t[:, 2] > 0]          # streaming warps (idle warps of the last CTA stop after rotation)
+    assert len(t) > 0
+    assert (t[:, 1] >= t[:, 0]).all() and (t[:, 2] >= t[:, 1]).all()
+    assert (t[:, 3] >= t[:, 2]).all() and (t[:, 4] >= t[:, 3]).all()
+    assert t[:, 5].sum() >= -(-cfg.units * (cfg.n_vis + cfg.n_text) // 64)  # >= #64-token tiles
