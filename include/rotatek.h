@@ -239,6 +239,29 @@ rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dims, int32_t r_units
                                        rotatek_stream_t stream);
 
 /*
+ * Variable-length units (a batch of VLM requests with different image-token / prompt
+ * counts, P:133-135 and NEXT-2; Alg. 2 per unit over that unit's own tokens): as
+ * rotatek_decode_attn_ex2 over caches padded to dims->n_vis / n_text rows per unit, with
+ *   n_vis_u  [U] int32 device (or NULL = n_vis for every unit): unit u attends to visual
+ *            rows [0, n_vis_u[u]) of K_comp[u] / V[u] only; values clamp to [0, n_vis]
+ *   n_text_u [U] int32 device (or NULL = n_text): text rows [0, n_text_u[u]) of K_text[u]
+ * Padding rows are streamed but masked out of the softmax (weight exactly 0); they must
+ * hold finite values (e.g. zeros: 0 * Inf/NaN would still poison the tensor-core P.V).
+ * A unit with no valid token at all has an undefined (NaN) output.  Units of a real batch
+ * would usually be packed by length order instead of padded; padding keeps one uniform
+ * [U, N, .] layout, so HBM traffic and time follow the padded sizes.
+ * Errors: as rotatek_decode_attn_ex2; ALIGN also for the length arrays.
+ */
+rotatek_status rotatek_decode_attn_varlen(const rotatek_dims* dims, int32_t r_units,
+                                          const int32_t* n_vis_u, const int32_t* n_text_u,
+                                          const void* q, const void* K_comp, const void* V,
+                                          const float* R, const float* dmu, const void* K_text,
+                                          const void* V_text, float softmax_scale, float* out,
+                                          void* workspace, size_t workspace_bytes,
+                                          int32_t splits, int32_t kernel,
+                                          rotatek_stream_t stream);
+
+/*
  * Calibration statistics, accumulated on the device (NEXT-3 offline calibrated rotation,
  * P:588 "precomputed from calibration data and reused across samples"; and the
  * calibration half of token-sharded prefill).  The fp64 state holds the sums

@@ -255,12 +255,16 @@ rotatek_status rotatek_compress_kv(const rotatek_dims* dm, const void* K, const 
   return rotatek_compress_kv_ex(dm, K, R, K_comp, 0u, stream);
 }
 
-rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dm, int32_t r_units, const void* q, const void* K_comp,
-                                      const void* V, const float* R, const float* dmu,
-                                      const void* K_text, const void* V_text, float softmax_scale,
-                                      float* out, void* workspace, size_t workspace_bytes,
-                                      int32_t splits, int32_t kernel, rotatek_stream_t stream) {
+rotatek_status rotatek_decode_attn_varlen(const rotatek_dims* dm, int32_t r_units,
+                                         const int32_t* n_vis_u, const int32_t* n_text_u,
+                                         const void* q, const void* K_comp, const void* V,
+                                         const float* R, const float* dmu, const void* K_text,
+                                         const void* V_text, float softmax_scale, float* out,
+                                         void* workspace, size_t workspace_bytes, int32_t splits,
+                                         int32_t kernel, rotatek_stream_t stream) {
   g_launches = 0;
+  if ((n_vis_u && !aligned16(n_vis_u)) || (n_text_u && !aligned16(n_text_u)))
+    return fail(ROTATEK_ERR_ALIGN, "length arrays not 16-byte aligned");
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   const int M = dm->n_text;
@@ -288,11 +292,23 @@ rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dm, int32_t r_units, 
   a.out = out;
   a.nR = r_units;
   a.overlap = overlap;
+  a.nvu = n_vis_u;
+  a.ntu = dm->n_text > 0 ? n_text_u : nullptr;
   int n = 0;
   if ((s = launched(rk::launch_decode(a, ws, splits, kernel, reinterpret_cast<cudaStream_t>(stream)), &n)))
     return s;
   g_launches = n;
   return ROTATEK_OK;
+}
+
+rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dm, int32_t r_units, const void* q, const void* K_comp,
+                                      const void* V, const float* R, const float* dmu,
+                                      const void* K_text, const void* V_text, float softmax_scale,
+                                      float* out, void* workspace, size_t workspace_bytes,
+                                      int32_t splits, int32_t kernel, rotatek_stream_t stream) {
+  return rotatek_decode_attn_varlen(dm, r_units, nullptr, nullptr, q, K_comp, V, R, dmu, K_text,
+                                    V_text, softmax_scale, out, workspace, workspace_bytes, splits,
+                                    kernel, stream);
 }
 
 rotatek_status rotatek_decode_attn_ex(const rotatek_dims* dm, const void* q, const void* K_comp,

@@ -55,7 +55,18 @@ struct DecodeParams {
   uint32_t* nslot = nullptr;            // work stealing: partial slots per unit
   int overlap = 0;                      // programmatic dependent launch (ROTATEK_DECODE_OVERLAP)
   int Ms = 0;                           // K_text / V_text rows per unit (text_stride)
+  const int32_t* nvu = nullptr;         // variable lengths: valid visual tokens per unit (or null)
+  const int32_t* ntu = nullptr;         // variable lengths: valid text tokens per unit (or null)
 };
+
+// tokens of tile (u, vis, t, tn) that lie inside the unit's valid length (variable-length
+// units over padded caches; every token when no lengths are given)
+__device__ __forceinline__ int valid_tn(const DecodeParams& p, int u, bool vis, int t, int tn) {
+  const int32_t* lens = vis ? p.nvu : p.ntu;
+  if (lens == nullptr) return tn;
+  const int v = __ldg(lens + u) - t;
+  return v <= 0 ? 0 : (v < tn ? v : tn);
+}
 
 // Programmatic dependent launch.  Every streaming decode lets the next kernel on the stream
 // launch early (it must then griddepcontrol.wait before reading out); with `overlap` the
@@ -138,8 +149,10 @@ __global__ void __launch_bounds__(kGenWarps * 32) decode_generic_kernel(DecodePa
   const int n0 = (int)((long long)p.N * split / splits), n1 = (int)((long long)p.N * (split + 1) / splits);
   const int m0 = (int)((long long)p.M * split / splits), m1 = (int)((long long)p.M * (split + 1) / splits);
   const int total = (n1 - n0) + (m1 - m0);
+  const int nv_u = p.nvu ? __ldg(p.nvu + u) : p.N, nt_u = p.ntu ? __ldg(p.ntu + u) : p.M;
   for (int idx = w; idx < total; idx += kGenWarps) {
     const bool vis = idx < n1 - n0;
+    if (vis ? (n0 + idx >= nv_u) : (m0 + idx - (n1 - n0) >= nt_u)) continue;  // padding
     const T* krow;
     const T* vrow;
     int kw;
@@ -354,7 +367,7 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   const int ctas = (pl.NW + aw - 1) / aw;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout, a.nR > 0 ? a.nR : a.U,
-                 nullptr, nullptr, a.overlap, a.Ms};
+                 nullptr, nullptr, a.overlap, a.Ms, a.nvu, a.ntu};
   if (!(a.overlap ? launch_overlap(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)
                   : launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, pl.cmax)))
     return -1;
@@ -384,7 +397,7 @@ static int launch_steal_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_
   const int cmax = steal_cmax(pl.cmax, a.N, a.M, claim);
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout,
-                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot, 0, a.Ms};
+                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot, 0, a.Ms, a.nvu, a.ntu};
   if (!launch(kern, ctas, WARPS * 32, C::SMEM, st, p, pl.NW, cmax, claim, claim)) return -1;
   return 1;
 }
@@ -506,7 +519,7 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
   const int cmax = STEAL ? steal_cmax(pl.cmax, a.N, a.M, claim) : pl.cmax;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, g_trace, aw, a.pout,
-                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot, a.overlap, a.Ms};
+                 a.nR > 0 ? a.nR : a.U, ws.desc, ws.nslot, a.overlap, a.Ms, a.nvu, a.ntu};
   if (!(a.overlap ? launch_overlap(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, cmax, claim)
                   : launch(kern, ctas, WARPS * 32, C::SMEM, st, maps, p, pl.NW, cmax, claim)))
     return -1;
@@ -592,7 +605,7 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
   if (S > ws.max_splits) S = ws.max_splits;
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, nullptr, 0, a.pout,
-                 a.nR > 0 ? a.nR : a.U, nullptr, nullptr, 0, a.Ms};
+                 a.nR > 0 ? a.nR : a.U, nullptr, nullptr, 0, a.Ms, a.nvu, a.ntu};
   size_t sm = ((size_t)a.G * a.d + (size_t)a.G * a.r + a.G + 2 * kGenWarps * a.G +
                (size_t)kGenWarps * a.G * a.d) * sizeof(float);
   dim3 grid(S, a.U);

@@ -387,7 +387,9 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     if (j == 0) RK_TRACE(2, gtime());
     const uint32_t sb = sbase + st * C::STAGE;
     const int mid = lane >> 3, r8 = lane & 7;
-    if (tl.vis) {
+    const int tv = valid_tn(p, tl.u, tl.vis, tl.t, tl.tn);  // variable lengths: mask padding
+    if (tv == 0) {
+    } else if (tl.vis) {
       float s[NbV::value][2];
 #pragma unroll
       for (int nb = 0; nb < NbV::value; ++nb) {
@@ -401,8 +403,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
           gqa::mma16816(d, aq[2 * kp + 1], b2, b3);
         }
         const int t0 = 8 * nb + 2 * c;
-        s[nb][0] = (t0 < tl.tn) ? d[0] + d[2] + bg : -CUDART_INF_F;
-        s[nb][1] = (t0 + 1 < tl.tn) ? d[1] + d[3] + bg : -CUDART_INF_F;
+        s[nb][0] = (t0 < tv) ? d[0] + d[2] + bg : -CUDART_INF_F;
+        s[nb][1] = (t0 + 1 < tv) ? d[1] + d[3] + bg : -CUDART_INF_F;
       }
       softmax_pv(NbV{}, s, sb + C::KB, C::VH);
     } else {
@@ -420,8 +422,8 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
           gqa::mma16816(d, ax[2 * kp + 1], b2, b3);
         }
         const int t0 = 8 * nb + 2 * c;
-        s[nb][0] = (t0 < tl.tn) ? d[0] + d[2] : -CUDART_INF_F;
-        s[nb][1] = (t0 + 1 < tl.tn) ? d[1] + d[3] : -CUDART_INF_F;
+        s[nb][0] = (t0 < tv) ? d[0] + d[2] : -CUDART_INF_F;
+        s[nb][1] = (t0 + 1 < tv) ? d[1] + d[3] : -CUDART_INF_F;
       }
       softmax_pv(NbX{}, s, sb + 2 * C::XH, C::XH);
     }

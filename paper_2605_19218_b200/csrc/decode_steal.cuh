@@ -212,21 +212,23 @@ __global__ void __launch_bounds__(WARPS * 32, MINB) decode_steal_kernel(DecodePa
     mbar_wait(&bar[st], (uint32_t)((j / STAGES) & 1));
     if (j == 0) RK_TRACE(2, gtime());
     const unsigned char* kbuf = base + st * C::STAGE;
-    if (tl.vis) {
+    const int tv = valid_tn(p, tl.u, tl.vis, tl.t, tl.tn);  // variable lengths: mask padding
+    if (tv == 0) {
+    } else if (tl.vis) {
       const unsigned char* vbuf = kbuf + C::TT_V * RK * C::S;
-      if (tl.tn == C::TT_V)
-        tile_compute<T, RK, C::TT_V, G, NACC, true, true>(kbuf, vbuf, tl.tn, qts, qreg, bs, pbuf,
+      if (tv == C::TT_V)
+        tile_compute<T, RK, C::TT_V, G, NACC, true, true>(kbuf, vbuf, tv, qts, qreg, bs, pbuf,
                                                           m, l, acc, lane);
       else
-        tile_compute<T, RK, C::TT_V, G, NACC, false, true>(kbuf, vbuf, tl.tn, qts, qreg, bs, pbuf,
+        tile_compute<T, RK, C::TT_V, G, NACC, false, true>(kbuf, vbuf, tv, qts, qreg, bs, pbuf,
                                                            m, l, acc, lane);
     } else {
       const unsigned char* vbuf = kbuf + C::TT_X * kD * C::S;
-      if (tl.tn == C::TT_X)
-        tile_compute<T, kD, C::TT_X, G, NACC, true, false>(kbuf, vbuf, tl.tn, qs, xreg, bs, pbuf,
+      if (tv == C::TT_X)
+        tile_compute<T, kD, C::TT_X, G, NACC, true, false>(kbuf, vbuf, tv, qs, xreg, bs, pbuf,
                                                            m, l, acc, lane);
       else
-        tile_compute<T, kD, C::TT_X, G, NACC, false, false>(kbuf, vbuf, tl.tn, qs, xreg, bs, pbuf,
+        tile_compute<T, kD, C::TT_X, G, NACC, false, false>(kbuf, vbuf, tv, qs, xreg, bs, pbuf,
                                                             m, l, acc, lane);
     }
     // refill this slot (the whole warp has consumed it)

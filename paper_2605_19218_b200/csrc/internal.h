@@ -83,6 +83,8 @@ struct DecodeArgs {
   int nR = 0;             // distinct rotations: unit u uses R[u % nR], dmu[u % nR] (0: nR = U)
   int overlap = 0;        // ROTATEK_DECODE_OVERLAP: programmatic dependent launch
   int Ms = 0;             // K_text / V_text rows per unit (text_stride; >= M)
+  const int32_t* nvu = nullptr;  // variable lengths (rotatek_decode_attn_varlen) or null
+  const int32_t* ntu = nullptr;
 };
 // kernel: 0 auto, 1 generic, 2 fast.  Returns launches, -1 launch error, -2 unsupported.
 int launch_merge_parts(int U, int G, int d, int P, const float* parts, float* out, cudaStream_t st);

@@ -74,6 +74,8 @@ def lib():
             L.rotatek_decode_attn_partial.argtypes = [dp, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz, vp]
             L.rotatek_decode_attn_ex2.argtypes = [dp, i32, vp, vp, vp, vp, vp, vp, vp, f, vp, vp, sz,
                                                   i32, i32, vp]
+            L.rotatek_decode_attn_varlen.argtypes = [dp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                                     f, vp, vp, sz, i32, i32, vp]
             L.rotatek_compress_kv_ex2.argtypes = [dp, i32, vp, vp, vp, u32, vp]
             L.rotatek_calib_accumulate.argtypes = [dp, u32, vp, vp, i32, vp, vp, sz, vp]
             L.rotatek_calibrate_from_state.argtypes = [dp, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
@@ -85,7 +87,7 @@ def lib():
                        "rotatek_decode_attn_ex", "rotatek_select_topr", "rotatek_decode_attn_partial",
                        "rotatek_merge_partials", "rotatek_decode_attn_ex2", "rotatek_compress_kv_ex2",
                        "rotatek_calib_accumulate", "rotatek_calibrate_from_state",
-                       "rotatek_gather_tokens"):
+                       "rotatek_gather_tokens", "rotatek_decode_attn_varlen"):
                 getattr(L, fn).restype = ctypes.c_int
             L.rotatek_status_string.argtypes = [ctypes.c_int]
             L.rotatek_status_string.restype = ctypes.c_char_p
@@ -306,11 +308,14 @@ def decode_attn(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, R: torch
                 dmu: torch.Tensor | None, K_text: torch.Tensor | None = None,
                 V_text: torch.Tensor | None = None, scale: float = 0.0,
                 out: torch.Tensor | None = None, *, splits: int = 0, kernel: int = KERNEL_AUTO,
-                n_text: int | None = None, ws: torch.Tensor | None = None,
+                n_text: int | None = None, n_vis_u: torch.Tensor | None = None,
+                n_text_u: torch.Tensor | None = None, ws: torch.Tensor | None = None,
                 stream=None) -> torch.Tensor:
     """Alg. 2 for all query heads: q [U, G, d], K_comp [U, N, r], V [U, N, d], R [U, d, r],
     dmu [U, d] | None, K_text/V_text [U, M_cap, d] | None -> out [U, G, d] f32.
-    n_text: the M <= M_cap valid full-d tokens (default M_cap): an appendable segment."""
+    n_text: the M <= M_cap valid full-d tokens (default M_cap): an appendable segment.
+    n_vis_u / n_text_u: int32 [U] device, per-unit valid lengths over padded caches
+    (rotatek_decode_attn_varlen)."""
     U, G, d = q.shape
     N, r = K_comp.shape[1], K_comp.shape[2]
     Mcap = 0 if K_text is None else K_text.shape[1]
@@ -322,7 +327,10 @@ def decode_attn(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, R: torch
         out = torch.empty((U, G, d), dtype=torch.float32, device=q.device)
     if ws is None:
         ws = workspace(dims, OP_DECODE, q.device)
-    _check(lib().rotatek_decode_attn_ex2(ctypes.byref(dims), nR if nR != U else 0, _ptr(q),
+    for lens in (n_vis_u, n_text_u):
+        assert lens is None or (lens.dtype == torch.int32 and lens.shape == (U,) and lens.is_cuda)
+    _check(lib().rotatek_decode_attn_varlen(ctypes.byref(dims), nR if nR != U else 0,
+                                         _ptr(n_vis_u), _ptr(n_text_u), _ptr(q),
                                          _ptr(K_comp), _ptr(V), _ptr(R), _ptr(dmu),
                                          _ptr(K_text) if M else None, _ptr(V_text) if M else None,
                                          float(scale), _ptr(out), _ptr(ws), ws.numel(), int(splits),
