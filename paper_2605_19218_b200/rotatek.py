@@ -18,7 +18,7 @@ import threading
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librotatek.so")
+LIB_PATH = os.environ.get("ROTATEK_LIB") or os.path.join(_HERE, "librotatek.so")  # A/B builds
 
 OK, ERR_NULL, ERR_DIMS, ERR_ALIGN, ERR_WORKSPACE, ERR_UNSUPPORTED, ERR_CUDA = range(7)
 BF16, F32 = 0, 1
