@@ -464,7 +464,10 @@ def run_ours(args):
                      # frac > 1 is possible: the measured peak is a read+write copy, this
                      # kernel is a read-dominated stream (99.7 % reads, ncu)
                      "algorithmic_bytes_per_launch": bytes_layer,
-                     "kernel": "rotatek decode (fast TMA-bulk warp-streaming kernel)"},
+                     "kernel": ("rotatek decode (decode_fast_kernel: cp.async.bulk warp streaming, "
+                                "CUDA cores)" if cfg.group == 1 else
+                                "rotatek decode (decode_gqa_kernel: tensor-map TMA warp streaming, "
+                                "mma.sync)")},
         "decode_tflops": round(decode_flops(cfg) / (us_layer * 1e-6) / 1e12, 3),
         "cpu_baseline": cpu,
         "e2e": e2e,
