@@ -22,6 +22,11 @@ for cfg in (CONFIGS["llava_b1"].with_(h_kv=2, n_vis=300, n_text=20),
         if kern == 4 and cfg.head_dim != 128:
             continue
         out = rk.decode_attn(*args, kernel=kern)
+        # variable per-unit lengths (masked tiles, all-padding tiles skipped)
+        nv = torch.tensor([max(1, cfg.n_vis - 37 * u) for u in range(cfg.units)], dtype=torch.int32).cuda()
+        nt = torch.tensor([(cfg.n_text * u) // max(1, cfg.units) for u in range(cfg.units)],
+                          dtype=torch.int32).cuda()
+        rk.decode_attn(*args, kernel=kern, n_vis_u=nv, n_text_u=nt)
     # token shards (partial states + merge), offline state + shared rotation
     half = cfg.n_vis // 2
     parts = torch.stack([rk.decode_attn_partial(args[0], Kc[:, :half].contiguous(), args[2][:, :half].contiguous(),
