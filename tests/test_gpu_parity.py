@@ -353,6 +353,21 @@ def test_full_size_sampled(rk, name, sample):
     ref_dec = orc.decode(sub["q"].f64(), to_np64(Kc[idx]), sub["V"].f64(), to_np64(cal["R"][idx]),
                          to_np64(cal["dmu"][idx]), sub["Ktext"].f64(), sub["Vtext"].f64())
     assert max_rel_err(to_np64(out[sample]), ref_dec) <= 1e-4
+    # variable per-unit lengths at full size (rotatek_decode_attn_varlen, same launch
+    # configuration): a batch of requests with fewer image / prompt tokens than the padding
+    rng = np.random.default_rng(11)
+    nv = rng.integers(cfg.n_vis // 2, cfg.n_vis + 1, cfg.units).astype(np.int32)
+    nt = rng.integers(1, M + 1, cfg.units).astype(np.int32)
+    out_v = rk.decode_attn(to_torch(w["q"]), Kc, to_torch(w["V"]), cal["R"], cal["dmu"],
+                           to_torch(w["Ktext"]), to_torch(w["Vtext"]),
+                           n_vis_u=torch.from_numpy(nv).cuda(), n_text_u=torch.from_numpy(nt).cuda())
+    torch.cuda.synchronize()
+    for j, u in enumerate(sample):
+        a, b = int(nv[u]), int(nt[u])
+        ref_u = orc.decode(sub["q"].f64()[j:j + 1], to_np64(Kc[u:u + 1, :a]), sub["V"].f64()[j:j + 1, :a],
+                           to_np64(cal["R"][u:u + 1]), to_np64(cal["dmu"][u:u + 1]),
+                           sub["Ktext"].f64()[j:j + 1, :b], sub["Vtext"].f64()[j:j + 1, :b])
+        assert max_rel_err(to_np64(out_v[u:u + 1]), ref_u) <= 1e-4, (name, u, a, b)
 
 
 # ------------------------------------------------------------------ tcgen05 vs CUDA-core paths
