@@ -100,6 +100,25 @@ def test_decode_errors(rk):
     assert call(kernel=5) == rk.ERR_DIMS
 
 
+def test_decode_varlen_errors(rk):
+    """rotatek_decode_attn_varlen: host validation of the length arrays and the shared
+    rotation (no compute call: nothing here reaches a kernel launch)."""
+    L = rk.lib()
+    vp = ctypes.c_void_p
+    d = rk.make_dims(4, 7, 128, 32, 100, 16, 0, rk.BF16)
+
+    def call(nv=0x9000, nt=0x9100, r_units=0, q=0x1000, nws=8):
+        return L.rotatek_decode_attn_varlen(ctypes.byref(d), r_units, vp(nv), vp(nt), vp(q),
+                                            vp(0x2000), vp(0x3000), vp(0x4000), vp(0x5000),
+                                            vp(0x6000), vp(0x6100), 0.0, vp(0x8000), vp(0x7000),
+                                            nws, 0, 0, None)
+    assert call(nv=0x9004) == rk.ERR_ALIGN
+    assert call(nt=0x9104) == rk.ERR_ALIGN
+    assert call(q=0) == rk.ERR_NULL
+    assert call(nws=8) == rk.ERR_WORKSPACE
+    assert call(nws=1 << 40, r_units=3) == rk.ERR_DIMS    # r_units must divide units
+
+
 def test_compress_and_select_errors(rk):
     L = rk.lib()
     vp = ctypes.c_void_p
