@@ -9,7 +9,13 @@ HDR := $(wildcard $(PKG)/csrc/*.cuh) $(wildcard $(PKG)/csrc/*.h) include/rotatek
 
 all: $(PKG)/librotatek.so oracle/liboracle.so
 
-build/%.o: $(PKG)/csrc/%.cu $(HDR)
+# decode_ring.o does not depend on the other decode kernels' headers (and vice versa)
+RING_HDR := $(PKG)/csrc/decode_ring.cuh
+BASE_HDR := $(filter-out $(RING_HDR),$(HDR))
+build/decode_ring.o: $(BASE_HDR) $(RING_HDR)
+build/decode.o build/api.o build/calibrate.o build/compress.o build/compress_tc.o build/cov_tc.o build/subspace.o: $(BASE_HDR)
+
+build/%.o: $(PKG)/csrc/%.cu
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

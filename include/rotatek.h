@@ -24,8 +24,10 @@
  *     shard of units is a pointer offset (u0 * per-unit stride).
  *   - Query head h of unit u is g = h - u*G (h_kv = floor(h / G)).
  *   - All tensor pointers are DEVICE pointers, 16-byte aligned.  Buffers are
- *     owned by the caller; the library allocates nothing and keeps no state
- *     between calls.
+ *     owned by the caller; the library allocates nothing and keeps no data
+ *     state between calls (the only per-thread state is the error string, the
+ *     launch count and the diagnostics hook of rotatek_debug_decode_trace;
+ *     kernel attributes are set once per device).
  *   - Every call validates its arguments on the host, then only ENQUEUES work
  *     on `stream`: no synchronisation, no allocation, CUDA-graph capturable.
  *     Numerical problems are reported per unit on the device through `info`.
@@ -36,6 +38,9 @@
  *     every call leaves its counter region zeroed again, so the same
  *     workspace can be reused (and graph-replayed) without re-zeroing.
  *     Concurrent calls on different streams need different workspaces.
+ *     A decode workspace's counter region sits at its start and its size
+ *     depends on `units` only, so one zeroed buffer serves every decode shape
+ *     with the same units whose rotatek_workspace_bytes() it covers.
  */
 #ifndef ROTATEK_H_
 #define ROTATEK_H_
@@ -209,10 +214,12 @@ rotatek_status rotatek_decode_attn(const rotatek_dims* dims, const void* q, cons
  * the same up to fp32 re-association for every split count (App. C "standard
  * online-softmax merge").  `kernel` forces the implementation:
  * 0 auto, 1 the generic kernel (any d, r, G), 2 the TMA-pipelined CUDA-core streaming
- * kernel, 3 the tensor-core GQA streaming kernel, 4 the streaming kernels with work
- * stealing (bf16, d = 128, r = 32, G in {1, 7}; merges in arrival order, so results are
- * reproducible to fp32 re-association, not bit for bit) -- UNSUPPORTED if the shape has
- * none.  Used by tests and benches.
+ * kernel, 3 the tensor-core GQA kernel (one CTA per SM streaming a shared TMA ring; bf16,
+ * d = 128, r in {32, 64}, G in {2, 4, 7, 8}), 4 the streaming kernels with work stealing
+ * (bf16, d = 128, r = 32, G in {1, 7}; merges in arrival order, so results are
+ * reproducible to fp32 re-association, not bit for bit), 5 the per-warp tensor-core GQA
+ * kernel of ABI version 1 (same shapes as 3) -- UNSUPPORTED if the shape has none.  Used
+ * by tests and benches.
  * OR ROTATEK_DECODE_OVERLAP into `kernel` to launch the streaming kernels as programmatic
  * dependents of the preceding work on `stream` (griddepcontrol): they start streaming the
  * cache while that work finishes and wait for it only before reading q and the workspace.
@@ -245,8 +252,9 @@ rotatek_status rotatek_decode_attn_ex2(const rotatek_dims* dims, int32_t r_units
  *   n_vis_u  [U] int32 device (or NULL = n_vis for every unit): unit u attends to visual
  *            rows [0, n_vis_u[u]) of K_comp[u] / V[u] only; values clamp to [0, n_vis]
  *   n_text_u [U] int32 device (or NULL = n_text): text rows [0, n_text_u[u]) of K_text[u]
- * Padding rows are streamed but masked out of the softmax (weight exactly 0); they must
- * hold finite values (e.g. zeros: 0 * Inf/NaN would still poison the tensor-core P.V).
+ * Padding rows are streamed but masked out of the softmax (weight exactly 0) and out of
+ * the P.V product (the tensor-core kernels zero masked V rows in shared memory), so they
+ * may hold anything, NaN/Inf included.
  * A unit with no valid token at all has an undefined (NaN) output.  Units of a real batch
  * would usually be packed by length order instead of padded; padding keeps one uniform
  * [U, N, .] layout, so HBM traffic and time follow the padded sizes.
@@ -361,7 +369,8 @@ int rotatek_last_launch_count(void);
  * >= 8 * (number of streaming warps) uint64 that subsequent decode launches of the
  * streaming kernels fill with per-warp %globaltimer stamps (start, after the query
  * rotation, first tile ready, loop end, end) and counters (tiles, units).  NULL
- * uninstalls.  The buffer is caller-owned; the library keeps only the pointer.
+ * uninstalls.  The buffer is caller-owned; the library keeps only the pointer,
+ * per CALLING THREAD (launches from other threads are not traced).
  */
 void rotatek_debug_decode_trace(void* device_buffer);
 

@@ -17,6 +17,14 @@ rotatek_status fail(rotatek_status s, const char* fmt, const char* what = "") {
   return s;
 }
 
+// every entry point starts here: reset the launch count and clear a stale (non-sticky)
+// runtime error left by the caller's earlier CUDA calls, so the per-launch checks
+// (cudaPeekAtLastError) only ever see this call's own launches
+void begin_call() {
+  g_launches = 0;
+  (void)cudaGetLastError();
+}
+
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
 rotatek_status check_dims(const rotatek_dims* dm) {
@@ -82,7 +90,7 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const v
                                  uint32_t* keep_mask, int32_t* keep_idx, float* R_full,
                                  int32_t* info, void* workspace, size_t workspace_bytes,
                                  rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   const int U = dm->units, G = dm->group, d = dm->head_dim, r = dm->rank, N = dm->n_vis,
@@ -122,7 +130,7 @@ rotatek_status rotatek_calibrate_subspace(const rotatek_dims* dm, uint32_t flags
                                           float ridge, float* R, float* dmu, float* ritz,
                                           int32_t* info, void* workspace, size_t workspace_bytes,
                                           rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   const int U = dm->units, G = dm->group, d = dm->head_dim, r = dm->rank, N = dm->n_vis,
@@ -160,7 +168,7 @@ rotatek_status rotatek_calibrate_subspace(const rotatek_dims* dm, uint32_t flags
 rotatek_status rotatek_calib_accumulate(const rotatek_dims* dm, uint32_t flags, const void* K,
                                         const void* Qw, int32_t state_units, double* state,
                                         void* workspace, size_t workspace_bytes, rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   const int U = dm->units, G = dm->group, d = dm->head_dim, N = dm->n_vis, W = dm->q_window;
@@ -193,7 +201,7 @@ rotatek_status rotatek_calibrate_from_state(const rotatek_dims* dm, uint32_t fla
                                             float* R, float* dmu, float* eigvals, uint32_t* keep_mask,
                                             int32_t* keep_idx, float* R_full, int32_t* info, void* workspace,
                                             size_t workspace_bytes, rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   const int U = dm->units, d = dm->head_dim, r = dm->rank;
@@ -222,7 +230,7 @@ rotatek_status rotatek_calibrate_from_state(const rotatek_dims* dm, uint32_t fla
 
 rotatek_status rotatek_compress_kv_ex2(const rotatek_dims* dm, int32_t r_units, const void* K, const float* R,
                                       void* K_comp, uint32_t flags, rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   if (!K || !R || !K_comp) return fail(ROTATEK_ERR_NULL, "K, R and K_comp are required");
@@ -262,7 +270,7 @@ rotatek_status rotatek_decode_attn_varlen(const rotatek_dims* dm, int32_t r_unit
                                          const void* V_text, float softmax_scale, float* out,
                                          void* workspace, size_t workspace_bytes, int32_t splits,
                                          int32_t kernel, rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   if ((n_vis_u && !aligned16(n_vis_u)) || (n_text_u && !aligned16(n_text_u)))
     return fail(ROTATEK_ERR_ALIGN, "length arrays not 16-byte aligned");
   rotatek_status s = check_dims(dm);
@@ -279,7 +287,7 @@ rotatek_status rotatek_decode_attn_varlen(const rotatek_dims* dm, int32_t r_unit
   if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
   const int overlap = (kernel & ROTATEK_DECODE_OVERLAP) ? 1 : 0;
   kernel &= ~ROTATEK_DECODE_OVERLAP;
-  if (kernel < 0 || kernel > 4) return fail(ROTATEK_ERR_DIMS, "kernel must be 0..4 (| ROTATEK_DECODE_OVERLAP)");
+  if (kernel < 0 || kernel > 5) return fail(ROTATEK_ERR_DIMS, "kernel must be 0..5 (| ROTATEK_DECODE_OVERLAP)");
   if (r_units < 0 || (r_units > 0 && dm->units % r_units != 0))
     return fail(ROTATEK_ERR_DIMS, "r_units must divide units (0: one rotation per unit)");
   rk::DecodeArgs a;
@@ -334,7 +342,7 @@ rotatek_status rotatek_decode_attn_partial(const rotatek_dims* dm, const void* q
                                            const void* K_text, const void* V_text, float softmax_scale,
                                            float* part, void* workspace, size_t workspace_bytes,
                                            rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   const int M = dm->n_text;
@@ -366,7 +374,7 @@ rotatek_status rotatek_decode_attn_partial(const rotatek_dims* dm, const void* q
 rotatek_status rotatek_gather_tokens(int32_t units, int32_t n_src, int32_t n_keep, int32_t row_bytes,
                                      const int32_t* keep_idx, const void* src, void* dst, int32_t* err,
                                      rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   if (units < 1 || n_src < 1 || n_keep < 1 || row_bytes < 16 || row_bytes % 16 != 0)
     return fail(ROTATEK_ERR_DIMS, "bad gather dims (row_bytes: positive multiple of 16)");
   if (!keep_idx || !src || !dst) return fail(ROTATEK_ERR_NULL, "keep_idx, src and dst are required");
@@ -382,7 +390,7 @@ rotatek_status rotatek_gather_tokens(int32_t units, int32_t n_src, int32_t n_kee
 
 rotatek_status rotatek_merge_partials(int32_t units, int32_t group, int32_t head_dim, int32_t nparts,
                                       const float* parts, float* out, rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   if (units < 1 || group < 1 || head_dim < 1 || head_dim > 256 || nparts < 1)
     return fail(ROTATEK_ERR_DIMS, "bad merge dims");
   if (!parts || !out) return fail(ROTATEK_ERR_NULL, "parts and out are required");
@@ -399,7 +407,7 @@ rotatek_status rotatek_merge_partials(int32_t units, int32_t group, int32_t head
 rotatek_status rotatek_select_topr(int32_t units, int32_t head_dim, int32_t rank,
                                    const float* eigvals, uint32_t* keep_mask, int32_t* keep_idx,
                                    int32_t* info, rotatek_stream_t stream) {
-  g_launches = 0;
+  begin_call();
   if (units < 1 || head_dim < 1 || head_dim > 256 || rank < 1 || rank > head_dim)
     return fail(ROTATEK_ERR_DIMS, "bad select dims");
   if (!eigvals || !keep_mask || !keep_idx) return fail(ROTATEK_ERR_NULL, "eigvals, keep_mask, keep_idx required");

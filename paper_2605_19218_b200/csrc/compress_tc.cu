@@ -189,11 +189,11 @@ static int launch_compress_tc_r(int U, int N, const void* K, const float* R, voi
   using C = CmpCfg<RK>;
   CUtensorMap map;
   if (!encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTM, 128)) return -2;
-  static bool attr = [] {
-    return cudaFuncSetAttribute(compress_tc_kernel<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) ==
-           cudaSuccess;
-  }();
-  (void)attr;
+  static int attr_slot[kMaxDevices];
+  once_per_device(attr_slot, [] {
+    cudaFuncSetAttribute(compress_tc_kernel<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    return 1;
+  });
   const int ntiles = (N + kTM - 1) / kTM;
   int parts = (2 * kNumSMs + U - 1) / U;
   if (parts > ntiles) parts = ntiles;

@@ -210,6 +210,9 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
       for (int j = 0; j < 64; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
       if (et < kDc) colpart[((size_t)u * parts + p) * kDc + et] = colsum_sm[et];
     }
+    // every epilogue warp is done reading colsum_sm before the next item's drain may
+    // overwrite it (write-after-read across items of this persistent CTA)
+    asm volatile("bar.sync 1, 256;" ::: "memory");
   }
     }  // items
   tc::fence_before();
@@ -266,10 +269,11 @@ int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, c
                   bool allow_fused) {
   CUtensorMap map;
   if (!encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTK, 128)) return -2;
-  static bool attr = [] {
-    return cudaFuncSetAttribute(cov_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem) == cudaSuccess;
-  }();
-  (void)attr;
+  static int attr_slot[kMaxDevices];
+  once_per_device(attr_slot, [] {
+    cudaFuncSetAttribute(cov_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
+    return 1;
+  });
   // persistent: one CTA per SM over the U * parts work items (the ring runs across items)
   const int nitems = U * ws.parts;
   const int grid = nitems < kNumSMs ? nitems : kNumSMs;

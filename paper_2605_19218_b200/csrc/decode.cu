@@ -28,66 +28,19 @@
 #include <cstring>
 #include <type_traits>
 
-#include "common.cuh"
-#include "internal.h"
-#include "tc_common.cuh"
+#include "decode_common.cuh"
 
 namespace rk {
 
-struct DecodeParams {
-  int U, G, d, r, N, M;
-  const void* q;
-  const void* Kc;
-  const void* V;
-  const float* R;
-  const float* dmu;
-  const void* Kt;
-  const void* Vt;
-  float sl;  // softmax scale * log2(e)
-  float* out;
-  uint32_t* counters;
-  float* partials;
-  unsigned long long* trace = nullptr;  // diagnostics: [NW][8] globaltimer stamps (or null)
-  int aw = 0;                           // active (streaming) warps per CTA (<= WARPS)
-  float* pout = nullptr;                // partial-state output [U][G][d+2] (token shards) or null
-  int nR = 0;                           // unit u uses R[u % nR], dmu[u % nR]
-  unsigned long long* desc = nullptr;   // work stealing: per-warp range descriptors
-  uint32_t* nslot = nullptr;            // work stealing: partial slots per unit
-  int overlap = 0;                      // programmatic dependent launch (ROTATEK_DECODE_OVERLAP)
-  int Ms = 0;                           // K_text / V_text rows per unit (text_stride)
-  const int32_t* nvu = nullptr;         // variable lengths: valid visual tokens per unit (or null)
-  const int32_t* ntu = nullptr;         // variable lengths: valid text tokens per unit (or null)
-};
-
-// tokens of tile (u, vis, t, tn) that lie inside the unit's valid length (variable-length
-// units over padded caches; every token when no lengths are given)
-__device__ __forceinline__ int valid_tn(const DecodeParams& p, int u, bool vis, int t, int tn) {
-  const int32_t* lens = vis ? p.nvu : p.ntu;
-  if (lens == nullptr) return tn;
-  const int v = __ldg(lens + u) - t;
-  return v <= 0 ? 0 : (v < tn ? v : tn);
-}
-
-// Programmatic dependent launch.  Every streaming decode lets the next kernel on the stream
-// launch early (it must then griddepcontrol.wait before reading out); with `overlap` the
-// decode itself was launched early and waits before its first read of q / workspace.
-__device__ __forceinline__ void pdl_launch_dependents() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
 // diagnostics stamp k of warp gw (lane 0 only; no-op unless a trace buffer is installed)
 #define RK_TRACE(k, v)                                                              \
   do {                                                                              \
     if (p.trace != nullptr && lane == 0 && w < p.aw) p.trace[(size_t)gw * 8 + (k)] = (v); \
   } while (0)
 
-static unsigned long long* g_trace = nullptr;
+// diagnostics hook of the CALLING THREAD (rotatek_debug_decode_trace); null unless a test or
+// tool installed a buffer, so ordinary calls share no state
+static thread_local unsigned long long* g_trace = nullptr;
 
 // max units one CTA's token range can touch (its query table must hold them all)
 static int cta_units_max(int U, int N, int M, int NW, int warps) {
@@ -258,14 +211,14 @@ struct FastPlan {
 constexpr int kMaxWarpsPerSM = 16;  // bound used to size the partial workspace
 
 static int num_sms() {
-  static int n = [] {
+  static int slot[kMaxDevices];
+  return once_per_device(slot, [] {
     int dev = 0, v = 0;
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
       v = kNumSMs;
     return v;
-  }();
-  return n;
+  });
 }
 
 static FastPlan fast_plan(int U, int N, int M, int warps_per_sm, int min_tokens = 64) {
@@ -310,42 +263,24 @@ size_t decode_ws_layout(int U, int G, int d, int r, int N, int M, void* base, De
   size_t gen = (size_t)U * G * smax * (d + 2) * 4;
   size_t fast = (size_t)U * steal_cmax(pl.cmax, N, M, kStealMin) * G * (d + 4) * 4;
   size_t part = gen > fast ? gen : fast;
+  // the regions that must be zero (or exhausted) on entry come first and their offsets
+  // depend on U only, so a caller may reuse one zero-filled buffer (grown when needed) for
+  // every shape with the same U; the scratch partials (no initial state) come last
   char* b = static_cast<char*>(base);
   size_t off = 0;
   DecodeWs w;
   w.counters = (uint32_t*)(b ? b + off : nullptr);
   off += al256((size_t)U * 4);
-  w.partials = (float*)(b ? b + off : nullptr);
-  off += al256(part);
-  w.desc = (unsigned long long*)(b ? b + off : nullptr);
-  off += al256((size_t)kMaxStealWarps * 8);
   w.nslot = (uint32_t*)(b ? b + off : nullptr);
   off += al256((size_t)U * 4);
+  w.desc = (unsigned long long*)(b ? b + off : nullptr);
+  off += al256((size_t)kMaxStealWarps * 8);
+  w.partials = (float*)(b ? b + off : nullptr);
+  off += al256(part);
+  w.partial_bytes = part;
   w.max_splits = smax;
   if (ws) *ws = w;
   return off;
-}
-
-template <typename Kern, typename... Args>
-static bool launch(Kern kern, int ctas, int threads, size_t smem, cudaStream_t st, Args... args) {
-  kern<<<ctas, threads, smem, st>>>(args...);
-  return cudaPeekAtLastError() == cudaSuccess;
-}
-
-// launch as a programmatic dependent of the preceding work on the stream
-template <typename Kern, typename... Args>
-static bool launch_overlap(Kern kern, int ctas, int threads, size_t smem, cudaStream_t st, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(ctas);
-  cfg.blockDim = dim3(threads);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, args...) == cudaSuccess;
 }
 
 template <typename T, int RK, int G, int WARPS, int STAGES, int TTV, int MINB>
@@ -353,14 +288,15 @@ static int launch_fast_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   using C = FastCfg<T, RK, G, WARPS, STAGES, TTV>;
   static_assert(C::SMEM <= 227 * 1024, "shared memory");
   auto kern = decode_fast_kernel<T, RK, G, WARPS, STAGES, TTV, MINB>;
-  static int ctas_per_sm = [&] {
+  static int cps_slot[kMaxDevices];
+  const int ctas_per_sm = once_per_device(cps_slot, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, WARPS * 32, C::SMEM) != cudaSuccess || n < 1)
       n = 1;
     if (n * WARPS > kMaxWarpsPerSM) n = kMaxWarpsPerSM / WARPS;
     return n < 1 ? 1 : n;
-  }();
+  });
   const FastPlan pl = fast_plan(a.U, a.N, a.M, ctas_per_sm * WARPS);
   const int aw = active_warps(a.U, a.N, a.M, pl.NW, WARPS, C::CAP);
   if (aw < 1) return -3;  // the CTA query table cannot hold one warp's units
@@ -380,14 +316,15 @@ static int launch_steal_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_
   using C = StealCfg<T, RK, G, WARPS, STAGES, TTV>;
   static_assert(C::SMEM <= 227 * 1024, "shared memory");
   auto kern = decode_steal_kernel<T, RK, G, WARPS, STAGES, TTV, MINB>;
-  static int ctas_per_sm = [&] {
+  static int cps_slot[kMaxDevices];
+  const int ctas_per_sm = once_per_device(cps_slot, [&] {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     int n = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, WARPS * 32, C::SMEM) != cudaSuccess || n < 1)
       n = 1;
     if (n * WARPS > kMaxWarpsPerSM) n = kMaxWarpsPerSM / WARPS;
     return n < 1 ? 1 : n;
-  }();
+  });
   const FastPlan pl = fast_plan(a.U, a.N, a.M, ctas_per_sm * WARPS);
   if (pl.NW > kMaxStealWarps || (long long)a.U * (a.N + a.M) >= (1LL << 31)) return -3;
   const int aw = active_warps(a.U, a.N, a.M, pl.NW, WARPS, C::CAP);
@@ -505,10 +442,11 @@ static int launch_gqa_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t 
     if (!encode_tmap_3d_bf16_strided(&maps.vt, a.Vt, kD, a.M, a.U, a.Ms, 64, C::TX, 128)) return -2;
   }
   auto kern = decode_gqa_kernel<RK, G, WARPS, TTV, STAGES, STEAL>;
-  static bool attr = [&] {
-    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM) == cudaSuccess;
-  }();
-  (void)attr;
+  static int attr_slot[kMaxDevices];
+  once_per_device(attr_slot, [&] {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    return 1;
+  });
   // >= 96 tokens per warp (fewer, longer ranges on small shapes: Qwen b1 26 -> 23 us)
   const FastPlan pl = fast_plan(a.U, a.N, a.M, WARPS, 96);
   if (STEAL && pl.NW > kMaxStealWarps) return -3;
@@ -589,13 +527,16 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
   }
   const bool fast_ok = fast_supported(a);
   const bool gqa_ok = gqa_supported(a);
-  if ((kernel == 2 && !fast_ok) || (kernel == 3 && !gqa_ok)) return -2;
+  if ((kernel == 2 && !fast_ok) || ((kernel == 3 || kernel == 5) && !gqa_ok)) return -2;
   // -3: the streaming kernels' CTA query table cannot hold the units of one CTA range
   // (tiny units, e.g. N + M < ~100 tokens); the generic kernel handles those shapes
   if (kernel == 3 || (kernel == 0 && gqa_ok && splits <= 0)) {
-    const int rc = a.r == 32 ? launch_gqa_rk<32>(a, ws, st) : launch_gqa_rk<64>(a, ws, st);
+    const int rc = launch_ring(a, ws, st);
     if (rc != -3) return rc;
     if (kernel == 3) return -2;
+  } else if (kernel == 5) {  // the per-warp GQA kernel of round 1 (decode_gqa.cuh), for A/B
+    const int rc = a.r == 32 ? launch_gqa_rk<32>(a, ws, st) : launch_gqa_rk<64>(a, ws, st);
+    return rc == -3 ? -2 : rc;
   } else if ((kernel == 0 && fast_ok && splits <= 0) || kernel == 2) {
     const int rc = a.bf16 ? launch_fast_rk<__nv_bfloat16>(a, ws, st) : launch_fast_rk<float>(a, ws, st);
     if (rc != -3) return rc;
@@ -653,5 +594,7 @@ int launch_merge_parts(int U, int G, int d, int P, const float* parts, float* ou
 }
 
 void set_decode_trace(void* buf) { g_trace = static_cast<unsigned long long*>(buf); }
+unsigned long long* decode_trace_buffer() { return g_trace; }
+int decode_num_sms() { return num_sms(); }
 
 }  // namespace rk

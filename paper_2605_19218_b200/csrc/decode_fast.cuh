@@ -16,17 +16,6 @@
 //     partials in slot order (deterministic) and re-arms the ticket.
 // No CTA-level barrier exists anywhere; the CTA is only a container of WARPS warps.
 
-constexpr int kD = 128;
-
-// Per-unit query table entry (see rotate_unit): qt [G][RK] f32 | b [G] f32 (16-B padded) |
-// q [G][kD] in the cache dtype.
-template <typename T, int RK, int G>
-struct QEnt {
-  static constexpr int OFF_B = G * RK * 4;
-  static constexpr int OFF_Q = OFF_B + ((G + 3) / 4) * 16;
-  static constexpr int BYTES = (OFF_Q + G * kD * (int)sizeof(T) + 15) / 16 * 16;
-};
-
 template <typename T, int RK, int G, int WARPS, int STAGES, int TTV>
 struct FastCfg {
   static constexpr int S = sizeof(T);

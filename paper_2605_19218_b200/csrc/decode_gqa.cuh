@@ -15,45 +15,6 @@
 // tcgen05 is not used here: with M = 2G <= 16 useful rows its 64/128-row tiles would waste
 // 4-8x of the tensor pipe, while the kernel is HBM-bound (~7 flop/byte).
 
-namespace gqa {
-
-__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
-               : "r"(addr));
-}
-__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-      "{%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-// element x0 -> low 16 bits, x1 -> high 16 bits
-__device__ __forceinline__ uint32_t pack2(float x0, float x1) {
-  __nv_bfloat162 v = __floats2bfloat162_rn(x0, x1);
-  return *reinterpret_cast<uint32_t*>(&v);
-}
-__device__ __forceinline__ void split2(float x0, float x1, uint32_t& hi, uint32_t& lo) {
-  const __nv_bfloat162 h = __floats2bfloat162_rn(x0, x1);
-  const float2 hf = __bfloat1622float2(h);
-  hi = *reinterpret_cast<const uint32_t*>(&h);
-  lo = pack2(x0 - hf.x, x1 - hf.y);
-}
-// byte offset of a 16-byte chunk in a row of a swizzled TMA box (rows of RB bytes)
-template <int RB>
-__device__ __forceinline__ uint32_t swz(uint32_t row, uint32_t chunk) {
-  const uint32_t off = row * RB + chunk * 16;
-  if constexpr (RB == 128) return off ^ (((off >> 7) & 7u) << 4);
-  else return off ^ (((off >> 7) & 3u) << 4);  // RB == 64: 64-byte swizzle
-}
-
-}  // namespace gqa
 
 template <int RK, int G, int WARPS, int TTV = 64, int STAGES = 1, bool STEAL = false>
 struct GqaCfg {
@@ -367,6 +328,19 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
     }
   };
 
+  // rows [t0, t1) of both 64-channel V halves (128-byte rows; the swizzle permutes chunks
+  // within a row only) set to zero: masked tokens get p = 0, and 0 * (padding NaN/Inf) would
+  // still poison the tensor-core P.V.
+  auto zero_rows = [&](unsigned char* v0, int half, int t0, int t1) {
+    const int n = (t1 - t0) * 8;  // 16-byte chunks per half
+    for (int i = lane; i < 2 * n; i += 32) {
+      const int h = i >= n, k = i - h * n;
+      reinterpret_cast<uint4*>(v0 + h * half + t0 * 128)[k] = make_uint4(0u, 0u, 0u, 0u);
+    }
+    fence_proxy_async();  // every writer: ordered before the stage's next TMA fill
+    __syncwarp();
+  };
+
   using NbV = std::integral_constant<int, C::TT / 8>;
   using NbX = std::integral_constant<int, C::TX / 8>;
 
@@ -406,6 +380,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
         s[nb][0] = (t0 < tv) ? d[0] + d[2] + bg : -CUDART_INF_F;
         s[nb][1] = (t0 + 1 < tv) ? d[1] + d[3] + bg : -CUDART_INF_F;
       }
+      if (tv < C::TT) zero_rows(base + st * C::STAGE + C::KB, C::VH, tv, C::TT);
       softmax_pv(NbV{}, s, sb + C::KB, C::VH);
     } else {
       float s[NbX::value][2];
@@ -425,6 +400,7 @@ __global__ void __launch_bounds__(WARPS * 32, 1) decode_gqa_kernel(const __grid_
         s[nb][0] = (t0 < tv) ? d[0] + d[2] : -CUDART_INF_F;
         s[nb][1] = (t0 + 1 < tv) ? d[1] + d[3] : -CUDART_INF_F;
       }
+      if (tv < C::TX) zero_rows(base + st * C::STAGE + 2 * C::XH, C::XH, tv, C::TX);
       softmax_pv(NbX{}, s, sb + 2 * C::XH, C::XH);
     }
     __syncwarp();

@@ -1,0 +1,810 @@
+// decode_ring.cuh -- the GQA decode kernel (G query heads per KV unit, 2 <= G <= 8; d = 128;
+// r in {32, 64}; bf16 cache), compiled in decode_ring.cu.
+//
+// Alg. 2 for every unit u and query head g, with the App. C split-K online
+// softmax.  Unlike decode_gqa_kernel (one private token range and ring per
+// WARP), the streaming unit here is the CTA, one per SM:
+//
+//  * Work split.  Every unit is cut into tiles -- ceil(N/64) visual tiles of 64 tokens, then
+//    ceil(M/32) text tiles of 32 full-d tokens -- and the U * tiles_per_unit tiles of the
+//    batch are split into one equal contiguous range per CTA.  Range ends fall on tile
+//    boundaries, so no tensor-map box reads past the range (partial boxes only at unit
+//    ends, where TMA zero-fills and moves no bytes).
+//  * Producer warp (one elected thread) walks the CTA's item sequence
+//        R-chunks of every unit the range touches, then the range's tiles in order
+//    through a ring of NSTG shared-memory stages (20 KB at r = 32: ~180 KB in flight per
+//    SM).  An R-chunk is 16 KB of R_r[u] rows (1-D bulk copies) plus, in a unit's first
+//    chunk, q[u] (G x 128 bf16) and dmu[u]: the rotation operands are the first bytes the
+//    CTA asks for, so the query rotation never queues behind the tile burst, and the tiles
+//    behind them stream while the rotation runs.  Tiles are tensor-map TMA boxes (K~ [64][r]
+//    with a 64/128-byte swizzle, V as two [64][64] 128-byte-swizzled halves; text K / V as
+//    halves) so ldmatrix reads them without bank conflicts.
+//  * Query rotation (Alg. 2 l.1-2) of all the CTA's units at once, by the eight consumer
+//    warps from the R-chunk stages: warp w sums rows [16w, 16w + 16) of q~ = q R_r and of
+//    b = q . dmu (x scale log2 e) for every head, the eight row partials are added in a fixed
+//    order (deterministic) into the CTA's query table.
+//  * Eight consumer warps = two GROUPS of four.  Group j takes the unit's tiles i with
+//    i % 2 == j; inside a group the four warps take the SAME tile: warp c scores tokens
+//    [16c, 16c + 16) -- S = A . K~^T with mma.sync.m16n8k16, A rows 0..G-1 = q~ rounded to
+//    bf16 (hi), rows 8..8+G-1 = the remainder (lo), so q~ enters with ~16 significant bits --
+//    the four row maxima meet in shared memory (one group barrier), each warp exponentiates
+//    its slice and publishes its P fragments (hi/lo rows, as for q~), and after a second
+//    group barrier warp c accumulates O[16 x 32] += P[16 x 64] . V[:, 32c .. 32c + 32).
+//    The four warps hold identical running maxima, so their row sums simply add at the unit
+//    end, where the two groups' states are merged through shared memory.  (Scoring the whole
+//    tile in every warp measured compute-bound: ~2 tiles/us/SM at any ring depth.)
+//  * Units spanning several CTAs: the unit's FIRST CTA (which reaches it at the END of its
+//    range) merges it.  Every other contributor -- reaching it at the START of its range, or
+//    holding it whole -- has group 0 write its merged partial (acc | m | l per head, slot =
+//    CTA - first CTA) and hands it to a FLUSHER warp that publishes it with a release
+//    reduction on the unit's counter, so no warp ever waits on a global round trip (one
+//    costs ~4-5 us under the decode's own load).  The merging CTA's flusher polls that
+//    counter while its consumers stream and prefetches the published partials, so at the
+//    end the merge (slot order: deterministic) needs no global round trip; it re-arms the
+//    counter (graph-replay safe).  The launch is COOPERATIVE (every CTA resident), so the
+//    merger's wait for a late contributor is a bounded spin.
+//  * Variable lengths: tiles past a unit's valid length are not loaded at all (the producer
+//    arrives on the stage without bytes), partially valid tiles are masked and their padded
+//    V rows zeroed in shared memory before the P.V product.
+//
+// Why: on Qwen-shaped caches (128 units, 4K tokens) the per-warp design lost ~18 us of a
+// 44 us launch to fixed costs (traces: rotation done at ~3 us, first tile at ~6 us, a 5 us
+// median spread of finish times between the warps of one SM, ~4 us of unit merges over
+// ~6 partials per unit).  Here the rotation rides the ring, the SM's warps share one stream
+// (no within-SM spread), a unit has at most ~3 CTA partials, and an in-range unit boundary
+// costs no global round trip (it cost ~4.5 us per boundary with the ticket and the rotation
+// in line on the compute warps: tools/time_decode.py --trace-ring).
+
+template <int RK, int G>
+struct RingCfg {
+  static constexpr int TT = 64;                      // visual tile tokens
+  static constexpr int TX = 32;                      // text tile tokens
+  static constexpr int KB = TT * RK * 2;             // K~ box bytes
+  static constexpr int VH = TT * 128;                // one 64-channel V half
+  static constexpr int XH = TX * 128;                // one 64-channel text half
+  static constexpr int STAGE = KB + 2 * VH;          // 20 KB (r = 32), 24 KB (r = 64)
+  static constexpr int RROWS = 16384 / (RK * 4);     // R_r rows per chunk (16 KB)
+  static constexpr int NCH = kD / RROWS;             // R chunks per unit (1 or 2)
+  static constexpr int OFF_RQ = RROWS * RK * 4;      // q [G][128] bf16 in chunk 0
+  static constexpr int OFF_RD = OFF_RQ + G * kD * 2; // dmu [128] f32 in chunk 0
+  static constexpr int CAP = NCH == 1 ? 4 : 2;       // units per CTA range (query table)
+  static constexpr int ENT = QEnt<__nv_bfloat16, RK, G>::BYTES;
+  static constexpr int XREC = 18;                    // exchanged floats per lane (16 acc, m, l)
+  static constexpr int XBYTES = 4 * XREC * 32 * 4;   // group exchange [4 quarters][XREC][32]
+  static constexpr int RSCR = 8 * G * (RK + 1) * 4;  // rotation partials [8 warps][G][RK + 1]
+  static constexpr int UNI = XBYTES > RSCR ? XBYTES : RSCR;
+  static constexpr int MLCAP = 288;                  // (slot, head) pairs the flusher's merge holds
+  static constexpr int PFMAX = 2;                    // partials the flusher prefetches (count - 1)
+  static constexpr int OFF_TAB = 0;                  // query table [CAP] entries
+  static constexpr int OFF_X = OFF_TAB + CAP * ENT;  // exchange / rotation scratch (union)
+  static constexpr int OFF_ML = OFF_X + UNI;         // flusher (m, l) table [MLCAP][2] f32
+  static constexpr int OFF_P = OFF_ML + MLCAP * 8;   // P fragments [2 groups][8 n-blocks][2][32] u32
+  static constexpr int OFF_MX = OFF_P + 2 * 8 * 2 * 32 * 4;  // tile row maxima [2][4 warps][8] f32
+  static constexpr int OFF_LT = OFF_MX + 2 * 4 * 8 * 4;      // unit row sums [2][4 warps][8] f32
+  static constexpr int OFF_BAR = OFF_LT + 2 * 4 * 8 * 4;     // full[16] | empty[16] | freq[CAP] | rot[CAP]
+  static constexpr int HDR = (OFF_BAR + (32 + 2 * CAP) * 8 + 1023) / 1024 * 1024;
+  static constexpr int NSTG0 = (227 * 1024 - 1024 - HDR) / STAGE;
+  static constexpr int NSTG = NSTG0 < 16 ? NSTG0 : 16;
+  static constexpr int SMEM = HDR + NSTG * STAGE + 1024;  // + alignment slack
+  static constexpr int THREADS = 10 * 32;                  // producer + 8 consumers + flusher
+  static_assert(STAGE % 1024 == 0 && KB % 1024 == 0, "stage alignment (swizzle atoms)");
+  static_assert(OFF_RD + kD * 4 <= STAGE && 4 * XH <= STAGE, "R-chunk / text tile fit a stage");
+  static_assert(NSTG >= CAP * NCH + 2, "ring must hold the R-chunks and tiles behind them");
+  static_assert(RK == 32 || RK == 64, "rank");
+  static_assert(G >= 2 && G <= 8, "group");
+};
+
+struct RingMaps {
+  CUtensorMap kc, v, kt, vt;
+};
+
+struct RingPlan {
+  long long T;   // tiles of the batch = U * tpu
+  int tpu;       // tiles per unit
+  int nvt;       // visual tiles per unit
+  int C;         // CTAs
+  int cmax;      // partial slots per unit
+  __host__ __device__ __forceinline__ long long start(int c) const { return T * c / C; }
+  // CTA whose range holds tile k: the largest c with start(c) <= k
+  __host__ __device__ __forceinline__ int cta_of(long long k) const { return (int)(((k + 1) * C - 1) / T); }
+  // CTAs whose ranges hold tiles of unit u
+  __host__ __device__ __forceinline__ int count(int u) const {
+    return cta_of((long long)(u + 1) * tpu - 1) - cta_of((long long)u * tpu) + 1;
+  }
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t phase) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(phase)
+      : "memory");
+  return ok != 0;
+}
+// (fence.sc.gpu, i.e. __threadfence, measured ~5 us per ticket under the decode's load)
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void red_add_relaxed_gpu(unsigned* p, unsigned v) {
+  asm volatile("red.relaxed.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void mbar_arrive_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+template <int RK, int G>
+__global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
+    decode_ring_kernel(const __grid_constant__ RingMaps maps, DecodeParams p, RingPlan pl) {
+  using C = RingCfg<RK, G>;
+  constexpr int NKS = RK / 16;  // score k-steps
+  constexpr int S = C::NSTG;
+  constexpr int kRec = kD + 4;  // partial record: acc[kD] | m | l | pad
+  extern __shared__ unsigned char rsm_raw[];
+  // 1024-byte aligned base (swizzle atoms), derived by pointer arithmetic on the __shared__
+  // array so every access below stays a shared-memory (LDS/STS) access, not a generic one
+  unsigned char* sm = rsm_raw + ((1024u - (smem_u32(rsm_raw) & 1023u)) & 1023u);
+  unsigned char* ring = sm + C::HDR;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
+  uint64_t* empty = full + 16;
+  uint64_t* freq = full + 32;
+  uint64_t* rotb = freq + C::CAP;  // unit k >= 1 rotated (by the flusher)
+  float* xch = reinterpret_cast<float*>(sm + C::OFF_X);
+  uint32_t* pbuf = reinterpret_cast<uint32_t*>(sm + C::OFF_P);
+  float* mxb = reinterpret_cast<float*>(sm + C::OFF_MX);
+  float* ltb = reinterpret_cast<float*>(sm + C::OFF_LT);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int N = p.N, M = p.M;
+  const int c_id = blockIdx.x;
+  const long long kA = pl.start(c_id), kB = pl.start(c_id + 1);
+  if (kA >= kB) return;
+  const int uA = (int)(kA / pl.tpu), uB = (int)((kB - 1) / pl.tpu);
+  const int nu = uB - uA + 1;  // <= CAP (host-checked)
+  // diagnostics (rotatek_debug_decode_trace): 16 stamps per CTA
+  const bool tr = p.trace != nullptr && lane == 0;
+  auto stamp = [&](int slot, unsigned long long v) {
+    if (tr) p.trace[(size_t)c_id * 16 + slot] = v;
+  };
+  if (warp == 1) stamp(0, gtime());
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 4);  // the four warps of the consuming group
+    }
+    for (int k = 0; k < C::CAP; ++k) {
+      mbar_init(&freq[k], 1);
+      mbar_init(&rotb[k], 1);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_launch_dependents();
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ producer
+    if (lane != 0) return;
+    if (p.overlap) pdl_wait();  // q is written by the preceding kernel
+    tc::prefetch_tmap(&maps.kc);
+    tc::prefetch_tmap(&maps.v);
+    if (M > 0) {
+      tc::prefetch_tmap(&maps.kt);
+      tc::prefetch_tmap(&maps.vt);
+    }
+    const uint64_t pol = policy_evict_first();
+    uint64_t pol_keep;  // rotation operands: a neighbouring CTA sharing the unit reads them too
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_keep));
+    int pos = 0;
+    auto acquire = [&](int& s) {
+      s = pos % S;
+      mbar_wait(&empty[s], ((pos / S) & 1) ^ 1);
+      return ring + s * C::STAGE;
+    };
+    for (int u = uA; u <= uB; ++u) {
+      const int ur = u % p.nR;
+      for (int ch = 0; ch < C::NCH; ++ch, ++pos) {
+        int s;
+        unsigned char* dst = acquire(s);
+        const uint32_t rb = C::RROWS * RK * 4;
+        const uint32_t qb = ch == 0 ? G * kD * 2 : 0, db = (ch == 0 && p.dmu) ? kD * 4 : 0;
+        mbar_arrive_expect_tx(&full[s], rb + qb + db);
+        bulk_g2s(dst, p.R + (size_t)ur * kD * RK + (size_t)ch * C::RROWS * RK, rb, &full[s], pol_keep);
+        if (qb) bulk_g2s(dst + C::OFF_RQ, static_cast<const __nv_bfloat16*>(p.q) + (size_t)u * G * kD, qb, &full[s], pol_keep);
+        if (db) bulk_g2s(dst + C::OFF_RD, p.dmu + (size_t)ur * kD, db, &full[s], pol_keep);
+      }
+    }
+    for (int u = uA; u <= uB; ++u) {
+      const long long k0 = (long long)u * pl.tpu;
+      const int ja = kA > k0 ? (int)(kA - k0) : 0;
+      const int jb = kB < k0 + pl.tpu ? (int)(kB - k0) : pl.tpu;
+      for (int j = ja; j < jb; ++j, ++pos) {
+      int s;
+      unsigned char* dst = acquire(s);
+      if (j < pl.nvt) {
+        const int t = j * C::TT;
+        const int tn = N - t < C::TT ? N - t : C::TT;
+        if (valid_tn(p, u, true, t, tn) == 0) {
+          mbar_arrive_cta(&full[s]);  // nothing valid: no bytes moved
+          continue;
+        }
+        mbar_arrive_expect_tx(&full[s], C::STAGE);
+        tc::tma_load_3d(dst, &maps.kc, 0, t, u, &full[s], pol);
+        tc::tma_load_3d(dst + C::KB, &maps.v, 0, t, u, &full[s], pol);
+        tc::tma_load_3d(dst + C::KB + C::VH, &maps.v, 64, t, u, &full[s], pol);
+      } else {
+        const int t = (j - pl.nvt) * C::TX;
+        const int tn = M - t < C::TX ? M - t : C::TX;
+        if (valid_tn(p, u, false, t, tn) == 0) {
+          mbar_arrive_cta(&full[s]);
+          continue;
+        }
+        mbar_arrive_expect_tx(&full[s], 4 * C::XH);
+        tc::tma_load_3d(dst, &maps.kt, 0, t, u, &full[s], pol);
+        tc::tma_load_3d(dst + C::XH, &maps.kt, 64, t, u, &full[s], pol);
+        tc::tma_load_3d(dst + 2 * C::XH, &maps.vt, 0, t, u, &full[s], pol);
+        tc::tma_load_3d(dst + 3 * C::XH, &maps.vt, 64, t, u, &full[s], pol);
+      }
+      }
+    }
+    return;
+  }
+
+  // the unit this CTA merges without a ticket when it can: the range's last unit, if the
+  // range holds its head and 1..PFMAX other CTAs hold the rest -- they reach that unit at the
+  // START of their ranges, so their partials are usually published long before this CTA's
+  // consumers get there, and the flusher prefetches them while the CTA streams
+  const int countB = pl.count(uB);
+  const bool merger = countB > 1 && pl.cta_of((long long)uB * pl.tpu) == c_id;
+  float* own = reinterpret_cast<float*>(ring);  // [G][kRec]: this CTA's state of unit uB (idle ring)
+
+  // ---------------- query rotation (Alg. 2 l.1-2) of unit k from its R-chunk stage(s), in one
+  // fixed summation order whoever computes it: 16-row block w of q~ = q R_r as a pairwise
+  // fmaf chain per lane (columns lane + 32 cc), and of b = q . dmu as a 16-lane shuffle tree;
+  // the eight block partials are added in order w = 0..7
+  using E = QEnt<__nv_bfloat16, RK, G>;
+  auto rot_chunks = [&](int k, const unsigned char* (&chs)[C::NCH]) {
+#pragma unroll
+    for (int ch = 0; ch < C::NCH; ++ch) {
+      const int ps = k * C::NCH + ch;  // R-chunks lead the ring: first lap
+      mbar_wait(&full[ps % S], 0);
+      chs[ch] = ring + (ps % S) * C::STAGE;
+    }
+  };
+  auto rot_block = [&](int w, const unsigned char* const (&chs)[C::NCH], float (&racc)[G][RK / 32], float (&bpart)[G]) {
+    const __nv_bfloat16* qs = reinterpret_cast<const __nv_bfloat16*>(chs[0] + C::OFF_RQ);
+    const int i0 = 16 * w;
+    const float* Rc = reinterpret_cast<const float*>(chs[i0 / C::RROWS]) + (size_t)(i0 % C::RROWS) * RK;
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg)
+#pragma unroll
+      for (int cc = 0; cc < RK / 32; ++cc) racc[gg][cc] = 0.f;
+#pragma unroll
+    for (int ii = 0; ii < 16; ii += 2) {
+      float r0[RK / 32], r1[RK / 32];
+#pragma unroll
+      for (int cc = 0; cc < RK / 32; ++cc) {
+        r0[cc] = Rc[ii * RK + lane + 32 * cc];
+        r1[cc] = Rc[(ii + 1) * RK + lane + 32 * cc];
+      }
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        const float2 qv = __bfloat1622float2(reinterpret_cast<const __nv_bfloat162*>(qs + gg * kD + i0 + ii)[0]);
+#pragma unroll
+        for (int cc = 0; cc < RK / 32; ++cc) racc[gg][cc] = fmaf(qv.y, r1[cc], fmaf(qv.x, r0[cc], racc[gg][cc]));
+      }
+    }
+    const float dmv = (p.dmu && lane < 16) ? reinterpret_cast<const float*>(chs[0] + C::OFF_RD)[i0 + lane] : 0.f;
+#pragma unroll
+    for (int gg = 0; gg < G; ++gg) {
+      float v = lane < 16 ? __bfloat162float(qs[gg * kD + i0 + lane]) * dmv : 0.f;
+      v += __shfl_xor_sync(0xffffffffu, v, 8);
+      v += __shfl_xor_sync(0xffffffffu, v, 4);
+      v += __shfl_xor_sync(0xffffffffu, v, 2);
+      v += __shfl_xor_sync(0xffffffffu, v, 1);
+      bpart[gg] = v;  // lane 0
+    }
+  };
+
+  if (warp == 9) {
+    // ------------------------------------------------------------------ flusher
+    // first: the rotations of units 1.. of the range, in the background of the consumers'
+    // first unit (their R-chunks landed with the first one's)
+    for (int k = 1; k < nu; ++k) {
+      const unsigned char* chs[C::NCH];
+      rot_chunks(k, chs);
+      float sum[G][RK / 32], sb[G];
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+        sb[gg] = 0.f;
+#pragma unroll
+        for (int cc = 0; cc < RK / 32; ++cc) sum[gg][cc] = 0.f;
+      }
+#pragma unroll 1
+      for (int w = 0; w < 8; ++w) {
+        float racc[G][RK / 32], bpart[G];
+        rot_block(w, chs, racc, bpart);
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          sb[gg] += bpart[gg];
+#pragma unroll
+          for (int cc = 0; cc < RK / 32; ++cc) sum[gg][cc] += racc[gg][cc];
+        }
+      }
+      unsigned char* ent = sm + C::OFF_TAB + k * C::ENT;
+      float* qt = reinterpret_cast<float*>(ent);
+      float* be = reinterpret_cast<float*>(ent + E::OFF_B);
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+#pragma unroll
+        for (int cc = 0; cc < RK / 32; ++cc) qt[gg * RK + lane + 32 * cc] = sum[gg][cc] * p.sl;
+        if (lane == 0) be[gg] = sb[gg] * p.sl;
+      }
+      const uint4* src = reinterpret_cast<const uint4*>(chs[0] + C::OFF_RQ);
+      uint4* dst = reinterpret_cast<uint4*>(ent + E::OFF_Q);
+      for (int e = lane; e < G * kD * 2 / 16; e += 32) dst[e] = src[e];
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive_cta(&rotb[k]);  // release: the table entry is written
+#pragma unroll
+        for (int ch = 0; ch < C::NCH; ++ch)
+          for (int a = 0; a < 4; ++a) mbar_arrive_cta(&empty[(k * C::NCH + ch) % S]);
+      }
+    }
+    // one request per unit of the range that spans several CTAs, in unit order.  Protocol
+    // (the launch is cooperative, so every CTA is resident and a bounded spin is safe): the
+    // unit's FIRST CTA merges it; every other contributor publishes its partial with a
+    // release reduction on the unit's counter and never waits for the result.
+    float* ml = reinterpret_cast<float*>(sm + C::OFF_ML);
+    int r = 0;
+    for (int u = uA; u <= uB; ++u) {
+      const int count = pl.count(u);
+      if (count == 1) continue;
+      float* part = p.partials + (size_t)u * pl.cmax * G * kRec;
+      if (!(u == uB && merger)) {
+        mbar_wait(&freq[r], 0);  // group 0's partial stores are ordered before this (bar + arrive)
+        ++r;
+        if (lane == 0) {
+          fence_acq_rel_gpu();  // cumulative: publishes the CTA's partial before the count
+          red_add_relaxed_gpu(&p.counters[u], 1u);
+        }
+        if (u == uA) stamp(10, gtime());
+        continue;
+      }
+      // ---- this CTA merges unit uB: prefetch the others' partials while the consumers stream
+      // (they reached this unit at the START of their ranges), wait only at the end if needed
+      float4 pv[C::PFMAX][G];
+      float pm[C::PFMAX][G], pl_[C::PFMAX][G];
+      const bool small = count - 1 <= C::PFMAX;
+      bool have = false;
+      auto arrived = [&] {
+        unsigned cnt = 0;
+        if (lane == 0) cnt = ld_acquire_gpu(&p.counters[u]);
+        return __shfl_sync(0xffffffffu, cnt, 0) == (unsigned)(count - 1);
+      };
+      auto prefetch = [&] {
+#pragma unroll
+        for (int s1 = 0; s1 < C::PFMAX; ++s1)
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+            const float* src = part + ((size_t)(s1 + 1) * G + gg) * kRec;
+            const bool in = s1 + 1 < count;
+            pv[s1][gg] = in ? __ldcg(reinterpret_cast<const float4*>(src) + lane) : make_float4(0.f, 0.f, 0.f, 0.f);
+            pm[s1][gg] = in ? __ldcg(src + kD) : -CUDART_INF_F;
+            pl_[s1][gg] = in ? __ldcg(src + kD + 1) : 0.f;
+          }
+        have = true;
+      };
+      while (small && !have && !mbar_test(&freq[r], 0)) {
+        if (arrived()) prefetch();
+        else __nanosleep(256);
+      }
+      mbar_wait(&freq[r], 0);  // this CTA's own state is in `own`
+      ++r;
+      while (!arrived()) __nanosleep(64);  // the other contributors (all resident)
+      if (small && !have) prefetch();
+      if (small) {
+        // merge in slot order (own = slot 0)
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          const float m0 = own[gg * kRec + kD], l0 = own[gg * kRec + kD + 1];
+          const float4 v0 = reinterpret_cast<const float4*>(own + gg * kRec)[lane];
+          float Mx = fmaxf(-CUDART_INF_F, m0);
+#pragma unroll
+          for (int s1 = 0; s1 < C::PFMAX; ++s1) Mx = fmaxf(Mx, pm[s1][gg]);
+          float f = (m0 == -CUDART_INF_F) ? 0.f : fast_exp2(m0 - Mx);
+          float Ls = fmaf(l0, f, 0.f);
+          float4 A = make_float4(fmaf(v0.x, f, 0.f), fmaf(v0.y, f, 0.f), fmaf(v0.z, f, 0.f), fmaf(v0.w, f, 0.f));
+#pragma unroll
+          for (int s1 = 0; s1 < C::PFMAX; ++s1) {
+            if (s1 + 1 >= count) continue;
+            f = (pm[s1][gg] == -CUDART_INF_F) ? 0.f : fast_exp2(pm[s1][gg] - Mx);
+            Ls = fmaf(pl_[s1][gg], f, Ls);
+            A.x = fmaf(pv[s1][gg].x, f, A.x);
+            A.y = fmaf(pv[s1][gg].y, f, A.y);
+            A.z = fmaf(pv[s1][gg].z, f, A.z);
+            A.w = fmaf(pv[s1][gg].w, f, A.w);
+          }
+          if (p.pout) {
+            float* po = p.pout + ((size_t)u * G + gg) * (kD + 2);
+            po[4 * lane] = A.x; po[4 * lane + 1] = A.y; po[4 * lane + 2] = A.z; po[4 * lane + 3] = A.w;
+            if (lane == 0) { po[kD] = Mx; po[kD + 1] = Ls; }
+          } else {
+            const float inv = 1.f / Ls;
+            reinterpret_cast<float4*>(p.out + ((size_t)u * G + gg) * kD)[lane] =
+                make_float4(A.x * inv, A.y * inv, A.z * inv, A.w * inv);
+          }
+        }
+      } else {
+        // many CTAs per unit (tiny batches): own state to slot 0, then the slot-order merge
+        for (int i = lane; i < G * kRec / 4; i += 32)
+          reinterpret_cast<float4*>(part)[i] = reinterpret_cast<const float4*>(own)[i];
+        __syncwarp();
+        for (int i = lane; i < count * G; i += 32) {
+          ml[2 * i] = __ldcg(part + (size_t)i * kRec + kD);
+          ml[2 * i + 1] = __ldcg(part + (size_t)i * kRec + kD + 1);
+        }
+        __syncwarp();
+        float Mx[G], Ls[G];
+        float4 A[G];
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          Mx[gg] = -CUDART_INF_F;
+          for (int s = 0; s < count; ++s) Mx[gg] = fmaxf(Mx[gg], ml[2 * (s * G + gg)]);
+          Ls[gg] = 0.f;
+          A[gg] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        for (int s0 = 0; s0 < count; ++s0) {
+          float4 v[G];
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg)
+            v[gg] = __ldcg(reinterpret_cast<const float4*>(part + ((size_t)s0 * G + gg) * kRec) + lane);
+#pragma unroll
+          for (int gg = 0; gg < G; ++gg) {
+            const int i = s0 * G + gg;
+            const float ms = ml[2 * i];
+            const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx[gg]);
+            Ls[gg] = fmaf(ml[2 * i + 1], f, Ls[gg]);
+            A[gg].x = fmaf(v[gg].x, f, A[gg].x);
+            A[gg].y = fmaf(v[gg].y, f, A[gg].y);
+            A[gg].z = fmaf(v[gg].z, f, A[gg].z);
+            A[gg].w = fmaf(v[gg].w, f, A[gg].w);
+          }
+        }
+#pragma unroll
+        for (int gg = 0; gg < G; ++gg) {
+          if (p.pout) {
+            float* po = p.pout + ((size_t)u * G + gg) * (kD + 2);
+            po[4 * lane] = A[gg].x; po[4 * lane + 1] = A[gg].y;
+            po[4 * lane + 2] = A[gg].z; po[4 * lane + 3] = A[gg].w;
+            if (lane == 0) { po[kD] = Mx[gg]; po[kD + 1] = Ls[gg]; }
+          } else {
+            const float inv = 1.f / Ls[gg];
+            reinterpret_cast<float4*>(p.out + ((size_t)u * G + gg) * kD)[lane] =
+                make_float4(A[gg].x * inv, A[gg].y * inv, A[gg].z * inv, A[gg].w * inv);
+          }
+        }
+      }
+      if (lane == 0) p.counters[u] = 0u;  // every other contributor has arrived: re-arm
+    }
+    stamp(4, gtime());
+    return;
+  }
+
+  // -------------------------------------------------------------------- consumers
+  const int ci = warp - 1;          // 0..7
+  const int grp = ci >> 2;          // tile parity this warp's group takes
+  const int qd = ci & 3;            // value-channel quarter [32 qd, 32 qd + 32)
+  const int ctid = threadIdx.x - 32;
+  const int g = lane >> 2, c = lane & 3, mid = lane >> 3, r8 = lane & 7;
+  const bool live = g < G;
+  const int gl = live ? g : 0;
+  const float z = live ? 1.f : 0.f;
+  if (p.overlap) pdl_wait();  // out / workspace may still be read by the preceding decode
+
+  int pos = 0;
+
+  // ---------------- query rotation of the range's first unit (all eight warps; the flusher
+  // rotates the others)
+  {
+    float* scr = xch;  // [8][G][RK + 1] row partials (the group exchange is not in use yet)
+    const unsigned char* chs[C::NCH];
+    rot_chunks(0, chs);
+    if (warp == 1) stamp(13, gtime());
+    {
+      float racc[G][RK / 32], bpart[G];
+      rot_block(ci, chs, racc, bpart);
+#pragma unroll
+      for (int gg = 0; gg < G; ++gg) {
+#pragma unroll
+        for (int cc = 0; cc < RK / 32; ++cc) scr[(ci * G + gg) * (RK + 1) + lane + 32 * cc] = racc[gg][cc];
+        if (lane == 0) scr[(ci * G + gg) * (RK + 1) + RK] = bpart[gg];
+      }
+    }
+    if (warp == 1) stamp(9, gtime());
+    named_bar(1, 256);
+    unsigned char* ent = sm + C::OFF_TAB;
+    float* qt = reinterpret_cast<float*>(ent);
+    float* be = reinterpret_cast<float*>(ent + E::OFF_B);
+    for (int o = ctid; o < G * (RK + 1); o += 256) {
+      float sum = 0.f;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) sum += scr[w * G * (RK + 1) + o];
+      const int gg = o / (RK + 1), jj = o % (RK + 1);
+      if (jj < RK) qt[gg * RK + jj] = sum * p.sl;
+      else be[gg] = sum * p.sl;
+    }
+    {  // raw q rows (the text keys use q)
+      const uint4* src = reinterpret_cast<const uint4*>(chs[0] + C::OFF_RQ);
+      uint4* dst = reinterpret_cast<uint4*>(ent + E::OFF_Q);
+      for (int e = ctid; e < G * kD * 2 / 16; e += 256) dst[e] = src[e];
+    }
+    named_bar(1, 256);  // table entry 0 written; scratch and stage reads done
+    if (grp == 0 && lane == 0)
+#pragma unroll
+      for (int ch = 0; ch < C::NCH; ++ch) mbar_arrive_cta(&empty[ch % S]);
+    pos += nu * C::NCH;  // the other units' R-chunks are the flusher's
+  }
+  if (warp == 1) stamp(1, gtime());
+
+  uint32_t aq[NKS][4];
+  float bg = 0.f, m = -CUDART_INF_F, l = 0.f;
+  float acc[4][4];
+  bool first_tile = true;
+  int nreq = 0;
+
+  // one tile, split over the group's four warps: this warp holds the scores s[NBW][2] (row g)
+  // of its NBW n-blocks (n-block nb0 + i); the tile's row maxima meet through shared memory,
+  // the exponentiated slice is published as P fragments, then O += P . V[:, quarter] over the
+  // NBT n-blocks of the tile
+  uint32_t* pgrp = pbuf + grp * (8 * 2 * 32);
+  float* mxg = mxb + grp * 32;
+  const int gbar = 7 + grp;  // named barrier of this group (128 threads)
+  auto softmax_pv = [&](auto nbw_tag, float (&s)[decltype(nbw_tag)::value][2], int nb0, int NBT, uint32_t v0,
+                        uint32_t vhalf) {
+    constexpr int NBW = decltype(nbw_tag)::value;
+    float tmax = -CUDART_INF_F;
+#pragma unroll
+    for (int j = 0; j < NBW; ++j) tmax = fmaxf(tmax, fmaxf(s[j][0], s[j][1]));
+    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
+    tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
+    if (c == 0) mxg[qd * 8 + g] = tmax;
+    named_bar(gbar, 128);
+    tmax = fmaxf(fmaxf(mxg[g], mxg[8 + g]), fmaxf(mxg[16 + g], mxg[24 + g]));
+    const float mn = live ? fmaxf(m, tmax) : 0.f;
+    // nothing valid yet keeps m = -inf: exp2(-inf - -inf) would be NaN
+    const bool ok = live && mn != -CUDART_INF_F;
+    const float alpha = ok ? fast_exp2(m - mn) : 0.f;
+    m = mn;
+    l *= alpha;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[j][e] *= alpha;
+#pragma unroll
+    for (int j = 0; j < NBW; ++j) {
+      const float p0 = ok ? fast_exp2(s[j][0] - mn) : 0.f;
+      const float p1 = ok ? fast_exp2(s[j][1] - mn) : 0.f;
+      l += p0 + p1;
+      uint32_t hi, lo;
+      gqa::split2(p0, p1, hi, lo);
+      pgrp[((nb0 + j) * 2 + 0) * 32 + lane] = hi;
+      pgrp[((nb0 + j) * 2 + 1) * 32 + lane] = lo;
+    }
+    named_bar(gbar, 128);
+    for (int kt = 0; kt < NBT / 2; ++kt) {
+      uint32_t pa[4];
+      pa[0] = pgrp[(4 * kt + 0) * 32 + lane];
+      pa[1] = pgrp[(4 * kt + 1) * 32 + lane];
+      pa[2] = pgrp[(4 * kt + 2) * 32 + lane];
+      pa[3] = pgrp[(4 * kt + 3) * 32 + lane];
+      const uint32_t tok = 16 * kt + r8 + 8 * (mid & 1);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const uint32_t cb = 4 * qd + 2 * h + (mid >> 1);  // 8-column block 0..15
+        const uint32_t addr = v0 + (cb >> 3) * vhalf + gqa::swz<128>(tok, cb & 7);
+        uint32_t b0, b1, b2, b3;
+        gqa::ldsm_x4_t(addr, b0, b1, b2, b3);
+        gqa::mma16816(acc[2 * h], pa, b0, b1);
+        gqa::mma16816(acc[2 * h + 1], pa, b2, b3);
+      }
+    }
+  };
+  // zero rows [t0, t1) of this warp's 32-column quarter of both V halves (128-byte rows):
+  // padding of variable-length units gets p = 0, but 0 * NaN would poison P.V
+  auto zero_rows = [&](unsigned char* v0, int half, int t0, int t1) {
+    const int hh = qd >> 1, cbase = 4 * (qd & 1);
+    for (int i = lane; i < (t1 - t0) * 4; i += 32) {
+      const int row = t0 + i / 4, ch = cbase + (i & 3);
+      *reinterpret_cast<uint4*>(v0 + hh * half + gqa::swz<128>(row, ch)) = make_uint4(0u, 0u, 0u, 0u);
+    }
+    fence_proxy_async();  // generic writes ordered before the stage's next TMA fill
+    __syncwarp();
+  };
+
+  for (int u = uA; u <= uB; ++u) {
+    if (u > uA) mbar_wait(&rotb[u - uA], 0);  // rotated by the flusher
+    const unsigned char* ent = sm + C::OFF_TAB + (u - uA) * C::ENT;
+    {  // per-unit state: A fragments of q~ (hi/lo rows), bias
+      const float* qts = reinterpret_cast<const float*>(ent);
+      const float2* t2 = reinterpret_cast<const float2*>(qts + gl * RK);
+#pragma unroll
+      for (int kk = 0; kk < NKS; ++kk) {
+        const float2 x0 = t2[8 * kk + c], x1 = t2[8 * kk + 4 + c];
+        gqa::split2(z * x0.x, z * x0.y, aq[kk][0], aq[kk][1]);
+        gqa::split2(z * x1.x, z * x1.y, aq[kk][2], aq[kk][3]);
+      }
+      bg = z * reinterpret_cast<const float*>(ent + E::OFF_B)[gl];
+      m = -CUDART_INF_F;
+      l = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[j][e] = 0.f;
+    }
+    const long long k0 = (long long)u * pl.tpu;
+    const long long ka = kA > k0 ? kA : k0, kb = kB < k0 + pl.tpu ? kB : k0 + pl.tpu;
+    for (long long k = ka; k < kb; ++k, ++pos) {
+      if (((int)(k - ka) & 1) != grp) continue;
+      const int st = pos % S;
+      mbar_wait(&full[st], (pos / S) & 1);
+      if (warp == 1 && first_tile) stamp(2, gtime());
+      if (warp == 1 && u == uA + 1 && k == ka) stamp(11, gtime());
+      first_tile = false;
+      unsigned char* stg = ring + st * C::STAGE;
+      const uint32_t sb = smem_u32(stg);
+      const int j = (int)(k - k0);
+      if (j < pl.nvt) {
+        const int t = j * C::TT;
+        const int tn = N - t < C::TT ? N - t : C::TT;
+        const int tv = valid_tn(p, u, true, t, tn);
+        if (tv > 0) {
+          constexpr int NBW = C::TT / 32;  // this warp's n-blocks: tokens [16 qd, 16 qd + 16)
+          float s[NBW][2];
+#pragma unroll
+          for (int i = 0; i < NBW; ++i) {
+            const int nb = NBW * qd + i;
+            float d[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint32_t row = 8 * nb + r8;
+#pragma unroll
+            for (int kp = 0; kp < RK / 32; ++kp) {
+              uint32_t b0, b1, b2, b3;
+              gqa::ldsm_x4(sb + gqa::swz<RK * 2>(row, 4 * kp + mid), b0, b1, b2, b3);
+              gqa::mma16816(d, aq[2 * kp], b0, b1);
+              gqa::mma16816(d, aq[2 * kp + 1], b2, b3);
+            }
+            const int t0 = 8 * nb + 2 * c;
+            s[i][0] = (t0 < tv) ? d[0] + d[2] + bg : -CUDART_INF_F;
+            s[i][1] = (t0 + 1 < tv) ? d[1] + d[3] + bg : -CUDART_INF_F;
+          }
+          if (tv < tn) zero_rows(stg + C::KB, C::VH, tv, tn);
+          softmax_pv(std::integral_constant<int, NBW>{}, s, NBW * qd, C::TT / 8, sb + C::KB, C::VH);
+        }
+      } else {
+        const int t = (j - pl.nvt) * C::TX;
+        const int tn = M - t < C::TX ? M - t : C::TX;
+        const int tv = valid_tn(p, u, false, t, tn);
+        if (tv > 0) {
+          // A fragments of q (x scale log2 e, hi/lo rows) from the table
+          uint32_t ax[8][4];
+          const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(ent + E::OFF_Q) + gl * (kD / 2);
+          const float zs = z * p.sl;
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const float2 lo = __bfloat1622float2(q2[8 * kk + c]), hi = __bfloat1622float2(q2[8 * kk + 4 + c]);
+            gqa::split2(zs * lo.x, zs * lo.y, ax[kk][0], ax[kk][1]);
+            gqa::split2(zs * hi.x, zs * hi.y, ax[kk][2], ax[kk][3]);
+          }
+          constexpr int NBW = C::TX / 32;  // this warp's n-blocks: tokens [8 qd, 8 qd + 8)
+          float s[NBW][2];
+#pragma unroll
+          for (int i = 0; i < NBW; ++i) {
+            const int nb = NBW * qd + i;
+            float d[4] = {0.f, 0.f, 0.f, 0.f};
+            const uint32_t row = 8 * nb + r8;
+#pragma unroll
+            for (int kp = 0; kp < 4; ++kp) {
+              const uint32_t chk = 4 * kp + mid;  // 16-byte chunk 0..15 of the 256-byte row
+              uint32_t b0, b1, b2, b3;
+              gqa::ldsm_x4(sb + (chk >> 3) * C::XH + gqa::swz<128>(row, chk & 7), b0, b1, b2, b3);
+              gqa::mma16816(d, ax[2 * kp], b0, b1);
+              gqa::mma16816(d, ax[2 * kp + 1], b2, b3);
+            }
+            const int t0 = 8 * nb + 2 * c;
+            s[i][0] = (t0 < tv) ? d[0] + d[2] : -CUDART_INF_F;
+            s[i][1] = (t0 + 1 < tv) ? d[1] + d[3] : -CUDART_INF_F;
+          }
+          if (tv < tn) zero_rows(stg + 2 * C::XH, C::XH, tv, tn);
+          softmax_pv(std::integral_constant<int, NBW>{}, s, NBW * qd, C::TX / 8, sb + 2 * C::XH, C::XH);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cta(&empty[st]);
+    }
+    // ---------------- unit end: merge the two groups, then write out or a CTA partial
+    // this warp's row sum covers its own token slices: the group's sum adds the four
+    float lt = l + __shfl_xor_sync(0xffffffffu, l, 1);
+    lt += __shfl_xor_sync(0xffffffffu, lt, 2);
+    if (c == 0) ltb[(grp * 4 + qd) * 8 + g] = lt;
+    float* xq = xch + qd * C::XREC * 32;
+    if (u == uA && (warp == 1 || warp == 5)) stamp(warp == 1 ? 8 : 12, gtime());
+    if (grp == 1) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) xq[(4 * j + e) * 32 + lane] = acc[j][e];
+      xq[16 * 32 + lane] = m;
+    }
+    named_bar(1, 256);  // group 1's state and every warp's row sum are in shared memory
+    if (grp == 1) {
+      named_bar(1, 256);  // ... and group 0 has read them: the buffers are free again
+      continue;
+    }
+    lt = (ltb[g] + ltb[8 + g]) + (ltb[16 + g] + ltb[24 + g]);
+    {
+      const float l1 = (ltb[32 + g] + ltb[40 + g]) + (ltb[48 + g] + ltb[56 + g]);
+      const float m1 = xq[16 * 32 + lane];
+      const float mn = fmaxf(m, m1);
+      const float f0 = (m == -CUDART_INF_F) ? 0.f : fast_exp2(m - mn);
+      const float f1 = (m1 == -CUDART_INF_F) ? 0.f : fast_exp2(m1 - mn);
+      m = mn;
+      lt = lt * f0 + l1 * f1;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[j][e] = acc[j][e] * f0 + xq[(4 * j + e) * 32 + lane] * f1;
+    }
+    named_bar(1, 256);
+    const int first = pl.cta_of(k0);
+    const int count = pl.count(u);
+    const int col = 32 * qd + 2 * c;  // + 8 j
+    if (count == 1) {
+      if (live) {
+        if (p.pout) {
+          float* po = p.pout + ((size_t)u * G + g) * (kD + 2);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<float2*>(po + col + 8 * j) = make_float2(acc[j][0] + acc[j][2], acc[j][1] + acc[j][3]);
+          if (qd == 0 && c == 0) { po[kD] = m; po[kD + 1] = lt; }
+        } else {
+          const float inv = 1.f / lt;
+          float* o = p.out + ((size_t)u * G + g) * kD + col;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            *reinterpret_cast<float2*>(o + 8 * j) =
+                make_float2((acc[j][0] + acc[j][2]) * inv, (acc[j][1] + acc[j][3]) * inv);
+        }
+      }
+      continue;
+    }
+    // the CTA's partial in slot (this CTA - first) -- or, for the unit this CTA merges itself,
+    // into the idle ring for the flusher -- then a request to the flusher warp
+    float* part = p.partials + (size_t)u * pl.cmax * G * kRec;
+    if (live) {
+      float* dst = (u == uB && merger) ? own + g * kRec : part + ((size_t)(c_id - first) * G + g) * kRec;
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        *reinterpret_cast<float2*>(dst + col + 8 * j) = make_float2(acc[j][0] + acc[j][2], acc[j][1] + acc[j][3]);
+      if (qd == 0 && c == 0) { dst[kD] = m; dst[kD + 1] = lt; }
+    }
+    named_bar(6, 128);  // group 0's partial stores precede the request
+    if (ci == 0 && lane == 0) mbar_arrive_cta(&freq[nreq]);
+    ++nreq;
+  }
+  if (warp == 1) {
+    stamp(3, gtime());
+    stamp(5, (unsigned long long)(kB - kA));
+    stamp(6, (unsigned long long)nu);
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    stamp(7, smid);
+  }
+}

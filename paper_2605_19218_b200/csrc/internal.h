@@ -8,6 +8,23 @@
 namespace rk {
 
 constexpr int kNumSMs = 148;
+constexpr int kMaxDevices = 64;
+
+// Once-per-(call site, device) setup: kernel attributes such as the >48 KB dynamic shared
+// memory opt-in are per-device state, so a process driving several GPUs must set them on
+// each.  slot[dev] caches init()'s (positive) result for the current device; a race between
+// threads only repeats the idempotent init.
+template <typename F>
+int once_per_device(int (&slot)[kMaxDevices], F&& init) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) return init();
+  int v = __atomic_load_n(&slot[dev], __ATOMIC_ACQUIRE);
+  if (v <= 0) {
+    v = init();
+    __atomic_store_n(&slot[dev], v, __ATOMIC_RELEASE);
+  }
+  return v;
+}
 
 struct CalibWs {
   double* sigma;     // [U, d]
@@ -27,6 +44,7 @@ struct DecodeWs {
   float* partials;     // [U, G, S, d + 2] (generic) or [U, cmax, G, d + 4] (streaming)
   unsigned long long* desc;  // [kMaxStealWarps] work-stealing range descriptors (left exhausted)
   uint32_t* nslot;           // [U] partial slots handed out per unit (zero on entry, left zero)
+  size_t partial_bytes;      // capacity of `partials`
   int max_splits;
 };
 constexpr int kMaxStealWarps = kNumSMs * 16;
@@ -91,5 +109,7 @@ int launch_merge_parts(int U, int G, int d, int P, const float* parts, float* ou
 void set_decode_trace(void* buf);  // diagnostics (rotatek_debug_decode_trace)
 int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kernel,
                   cudaStream_t st);
+// the CTA-ring GQA kernel (decode_ring.cu); -3: shape not served (caller falls back)
+int launch_ring(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st);
 
 }  // namespace rk

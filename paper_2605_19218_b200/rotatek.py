@@ -25,7 +25,7 @@ BF16, F32 = 0, 1
 CENTER, QUERY_WEIGHT, EIG_FP64, SIMT_ONLY = 1, 2, 4, 256
 DEFAULT_FLAGS = CENTER | QUERY_WEIGHT
 OP_CALIBRATE, OP_DECODE = 0, 1
-KERNEL_AUTO, KERNEL_GENERIC, KERNEL_FAST, KERNEL_GQA, KERNEL_STEAL = 0, 1, 2, 3, 4
+KERNEL_AUTO, KERNEL_GENERIC, KERNEL_FAST, KERNEL_GQA, KERNEL_STEAL, KERNEL_GQA_WARP = 0, 1, 2, 3, 4, 5
 DECODE_OVERLAP = 0x100  # OR into kernel: programmatic dependent launch (include/rotatek.h)
 
 
@@ -135,6 +135,19 @@ def _ptr(t):
     return ctypes.c_void_p(t.data_ptr())
 
 
+def _check_decode_dtypes(q, K_comp, V, R, dmu, K_text, V_text):
+    """The ABI reads q, V and the text K/V as K_comp's dtype and R, dmu as fp32: reject a
+    mismatch here instead of letting the kernel reinterpret the bytes."""
+    dt = K_comp.dtype
+    for name, t in (("q", q), ("V", V), ("K_text", K_text), ("V_text", V_text)):
+        if t is not None and t.dtype != dt:
+            raise TypeError(f"{name} is {t.dtype} but K_comp is {dt}: all cache tensors and q "
+                            "must share one dtype")
+    for name, t in (("R", R), ("dmu", dmu)):
+        if t is not None and t.dtype != torch.float32:
+            raise TypeError(f"{name} must be float32 (got {t.dtype})")
+
+
 def _stream(stream):
     s = torch.cuda.current_stream() if stream is None else stream
     return ctypes.c_void_p(s.cuda_stream)
@@ -153,16 +166,27 @@ def workspace_bytes(dims: Dims, op: int) -> int:
 _ws_cache: dict = {}
 
 
-def workspace(dims: Dims, op: int, device) -> torch.Tensor:
-    """Zero-filled workspace (the ABI requires zero on first use; calls leave it zeroed).
-    Cached per (device, op, size) for the current thread's stream."""
+def workspace(dims: Dims, op: int, device, stream=None) -> torch.Tensor:
+    """Zero-filled workspace for calls enqueued on `stream` (default: the current stream).
+
+    The ABI requires zeros on first use and every call leaves the counter region zeroed
+    (include/rotatek.h), so one buffer is kept per (device, op, stream, units) -- calls on
+    different streams never share counters -- and replaced by a larger zero-filled one
+    (allocated and zeroed ON that stream) when a shape needs more, e.g. an appendable text
+    segment growing during generation.  The decode counter region's offsets depend on the
+    unit count only, so a larger buffer serves every smaller shape of the same units."""
     n = workspace_bytes(dims, op)
     if n == 0:
         _check(ERR_DIMS)
-    key = (str(device), op, n, torch.cuda.current_stream(device).cuda_stream)
+    dev = torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    s = torch.cuda.current_stream(dev) if stream is None else stream
+    key = (str(dev), op, s.cuda_stream, int(dims.units) if op == OP_DECODE else 0)
     t = _ws_cache.get(key)
-    if t is None:
-        t = torch.zeros(n, dtype=torch.uint8, device=device)
+    if t is None or t.numel() < n:
+        with torch.cuda.stream(s):
+            t = torch.zeros(max(n, 0 if t is None else t.numel()), dtype=torch.uint8, device=dev)
         _ws_cache[key] = t
     return t
 
@@ -192,7 +216,7 @@ def calibrate(K: torch.Tensor, Qw: torch.Tensor | None, rank: int, flags: int = 
     )
     out["R_full"] = torch.empty((U, d, d), dtype=torch.float32, device=dev) if want_full else None
     if ws is None:
-        ws = workspace(dims, OP_CALIBRATE, dev)
+        ws = workspace(dims, OP_CALIBRATE, dev, stream)
     _check(lib().rotatek_calibrate(ctypes.byref(dims), flags, _ptr(K),
                                    _ptr(Qw) if W > 0 else None, _ptr(out["R"]), _ptr(out["dmu"]),
                                    _ptr(out["eigvals"]), _ptr(out["mask"]), _ptr(out["idx"]),
@@ -220,7 +244,7 @@ def calibrate_subspace(K: torch.Tensor, Qw: torch.Tensor | None, V0: torch.Tenso
                ritz=torch.empty((U, r), dtype=torch.float32, device=dev),
                info=torch.empty((U,), dtype=torch.int32, device=dev))
     if ws is None:
-        ws = workspace(dims, OP_CALIBRATE, dev)
+        ws = workspace(dims, OP_CALIBRATE, dev, stream)
     _check(lib().rotatek_calibrate_subspace(
         ctypes.byref(dims), flags, _ptr(K), _ptr(Qw) if W > 0 else None, _ptr(V0), int(iters),
         float(ridge), _ptr(out["R"]), _ptr(out["dmu"]), _ptr(out["ritz"]), _ptr(out["info"]),
@@ -252,7 +276,7 @@ def calib_accumulate(K: torch.Tensor, Qw: torch.Tensor | None, state: torch.Tens
     assert state.shape == (nS, state_doubles(d)) and state.dtype == torch.float64
     dims = make_dims(U, G, d, 1, N, 0, W, _dtype_code(K))
     if ws is None:
-        ws = workspace(dims, OP_CALIBRATE, K.device)
+        ws = workspace(dims, OP_CALIBRATE, K.device, stream)
     _check(lib().rotatek_calib_accumulate(ctypes.byref(dims), flags, _ptr(K),
                                           _ptr(Qw) if W > 0 else None, nS, _ptr(state), _ptr(ws),
                                           ws.numel(), _stream(stream)))
@@ -278,7 +302,7 @@ def calibrate_from_state(state: torch.Tensor, rank: int, flags: int = DEFAULT_FL
     )
     out["R_full"] = torch.empty((nS, d, d), dtype=torch.float32, device=dev) if want_full else None
     if ws is None:
-        ws = workspace(dims, OP_CALIBRATE, dev)
+        ws = workspace(dims, OP_CALIBRATE, dev, stream)
     _check(lib().rotatek_calibrate_from_state(
         ctypes.byref(dims), flags, _ptr(state), _ptr(out["R"]), _ptr(out["dmu"]),
         _ptr(out["eigvals"]), _ptr(out["mask"]), _ptr(out["idx"]), _ptr(out["R_full"]),
@@ -322,11 +346,12 @@ def decode_attn(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, R: torch
     M = Mcap if n_text is None else int(n_text)
     nR = R.shape[0]   # nR < U: shared (offline) rotation, unit u uses R[u % nR], dmu[u % nR]
     assert V.shape == (U, N, d) and R.shape == (nR, d, r) and U % nR == 0
+    _check_decode_dtypes(q, K_comp, V, R, dmu, K_text, V_text)
     dims = make_dims(U, G, d, r, N, M, 0, _dtype_code(K_comp), Mcap if M else 0)
     if out is None:
         out = torch.empty((U, G, d), dtype=torch.float32, device=q.device)
     if ws is None:
-        ws = workspace(dims, OP_DECODE, q.device)
+        ws = workspace(dims, OP_DECODE, q.device, stream)
     for lens in (n_vis_u, n_text_u):
         assert lens is None or (lens.dtype == torch.int32 and lens.shape == (U,) and lens.is_cuda)
     _check(lib().rotatek_decode_attn_varlen(ctypes.byref(dims), nR if nR != U else 0,
@@ -349,11 +374,12 @@ def decode_attn_partial(q: torch.Tensor, K_comp: torch.Tensor, V: torch.Tensor, 
     N, r = K_comp.shape[1], K_comp.shape[2]
     M = 0 if K_text is None else K_text.shape[1]
     assert V.shape == (U, N, d) and R.shape == (U, d, r)
+    _check_decode_dtypes(q, K_comp, V, R, dmu, K_text, V_text)
     dims = make_dims(U, G, d, r, N, M, 0, _dtype_code(K_comp))
     if part is None:
         part = torch.empty((U, G, d + 2), dtype=torch.float32, device=q.device)
     if ws is None:
-        ws = workspace(dims, OP_DECODE, q.device)
+        ws = workspace(dims, OP_DECODE, q.device, stream)
     _check(lib().rotatek_decode_attn_partial(ctypes.byref(dims), _ptr(q), _ptr(K_comp), _ptr(V),
                                              _ptr(R), _ptr(dmu), _ptr(K_text) if M else None,
                                              _ptr(V_text) if M else None, float(scale), _ptr(part),

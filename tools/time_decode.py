@@ -22,6 +22,7 @@ def alg_bytes(U, G, N, M, r, d=128, s=2):
 
 
 def time_shape(U, G, N, M, r, d=128, reps=30, kernel=0):
+    kernel |= int(os.environ.get("TD_OVERLAP", "0")) * rk.DECODE_OVERLAP
     b = alg_bytes(U, G, N, M, r)
     L = max(2, min(16, int(600e6 // b) + 1))
     dev = "cuda"
@@ -112,6 +113,69 @@ def trace_shape(U, G, N, M, r, d=128, kernel=0):
         print("   slowest SMs:", order[-8:].tolist(), " fastest:", order[:8].tolist())
 
 
+def trace_ring(U, G, N, M, r, d=128):
+    """The CTA-ring GQA kernel (kernel 3): 16 stamps per CTA (decode_ring.cuh) -> phase
+    times of the first unit boundary inside a CTA's range."""
+    dev = "cuda"
+    lay = []
+    for _ in range(2):
+        lay.append((torch.randn(U, G, d, device=dev).bfloat16(),
+                    torch.randn(U, N, r, device=dev).bfloat16(),
+                    torch.randn(U, N, d, device=dev).bfloat16(),
+                    torch.randn(U, d, r, device=dev) * 0.1, torch.randn(U, d, device=dev) * 0.1,
+                    torch.randn(U, M, d, device=dev).bfloat16() if M else None,
+                    torch.randn(U, M, d, device=dev).bfloat16() if M else None,
+                    torch.empty(U, G, d, device=dev)))
+    ws = rk.workspace(rk.make_dims(U, G, d, r, N, M), rk.OP_DECODE, dev)
+    buf = torch.zeros(148 * 16, dtype=torch.int64, device=dev)
+    for lay_ in lay:
+        rk.decode_attn(*lay_[:7], out=lay_[7], ws=ws, kernel=3)
+    torch.cuda.synchronize()
+    rk.debug_decode_trace(buf)
+    rk.decode_attn(*lay[0][:7], out=lay[0][7], ws=ws, kernel=3)
+    rk.decode_attn(*lay[1][:7], out=lay[1][7], ws=ws, kernel=3)
+    torch.cuda.synchronize()
+    rk.debug_decode_trace(None)
+    t = buf.view(-1, 16).cpu()
+    if os.environ.get("TD_DUMP"):
+        torch.save(t, os.environ["TD_DUMP"])
+    t = t[t[:, 0] > 0].double()
+    t0 = t[:, 0].min()
+    rel = lambda k: (t[:, k] - t0) / 1e3  # noqa: E731
+    q = torch.tensor([0.0, 0.5, 0.9, 1.0], dtype=torch.double)
+    tpu = -(-N // 64) + -(-M // 32)
+    T = U * tpu
+    C = t.shape[0]
+    print(f"ring trace U={U} G={G} N={N} M={M} r={r}: CTAs={C} tiles/CTA {T / C:.1f}")
+    for k, nm in [(13, "R0 landed"), (14, "R last landed"), (9, "rot0 partial"), (15, "rot0 bar"), (1, "rotated"), (2, "tile0"), (8, "u0 g0 done"),
+                  (12, "u0 g1 done"), (10, "u0 ticket"), (11, "u1 tile0"), (3, "consumers end"),
+                  (4, "flusher end")]:
+        v = rel(k)
+        v = v[t[:, k] > 0]
+        if v.numel() == 0:
+            continue
+        qq = torch.quantile(v, q).tolist()
+        print(f"   {nm:11s} min {qq[0]:7.2f}  med {qq[1]:7.2f}  p90 {qq[2]:7.2f}  max {qq[3]:7.2f} us  (n={v.numel()})")
+    two = t[:, 6] >= 2
+    if two.any():
+        c = torch.arange(C, dtype=torch.double)[two]
+        kA = torch.floor(c * T / C)
+        kB = torch.floor((c + 1) * T / C)
+        u0_tiles = torch.minimum(kB, (torch.floor(kA / tpu) + 1) * tpu) - kA
+        u1_tiles = (kB - kA) - u0_tiles
+        r0 = u0_tiles / (rel(8)[two] - rel(2)[two])
+        r1 = u1_tiles / (rel(3)[two] - rel(11)[two])
+        print(f"   2-unit CTAs: unit-0 tiles med {u0_tiles.median():.0f}; tiles/us unit 0 med {r0.median():.2f}, "
+              f"unit 1 med {r1.median():.2f};  boundary (g0 done -> u1 tile0) med "
+              f"{(rel(11)[two] - rel(8)[two]).median():.2f} us; flush med {(rel(9)[two] - rel(8)[two]).median():.2f}; "
+              f"g1 - g0 done med {(rel(12)[two] - rel(8)[two]).median():.2f}")
+    one = t[:, 6] == 1
+    if one.any():
+        c = torch.arange(C, dtype=torch.double)[one]
+        n = torch.floor((c + 1) * T / C) - torch.floor(c * T / C)
+        print(f"   1-unit CTAs: tiles/us med {(n / (rel(3)[one] - rel(2)[one])).median():.2f}")
+
+
 def trace_repeat(U, G, N, M, r, d=128, reps=3):
     """Is the per-warp finish time systematic?  Same launch traced `reps` times."""
     dev = "cuda"
@@ -166,6 +230,10 @@ def main():
     if sys.argv[1:2] == ["--repeat"]:
         for sh in sys.argv[2:]:
             trace_repeat(*(int(x) for x in sh.split(",")))
+        return
+    if sys.argv[1:2] == ["--trace-ring"]:
+        for sh in sys.argv[2:]:
+            trace_ring(*(int(x) for x in sh.split(",")))
         return
     if sys.argv[1:2] == ["--trace"]:
         for sh in sys.argv[2:]:
