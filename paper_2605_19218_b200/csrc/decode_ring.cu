@@ -21,7 +21,17 @@ static int launch_ring_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   const int sms = decode_num_sms();
   // CTAs: one per SM, fewer when a unit would span more CTAs than the merge's shared
   // (m, l) table holds (tiny batches, e.g. 4 units on 148 SMs)
-  for (pl.C = pl.T < sms ? (int)pl.T : sms;; --pl.C) {
+  // at least ceil(tpu / div) tiles per CTA (default div 6: a unit spans <= 7 CTAs, so its
+  // merge stays a few slots; tiny batches then use fewer SMs, each with a deeper stream --
+  // Qwen b1 (4 units) 31.4 -> 18.4 us, b8 20.6 us; b32 / long unchanged; tools/time_decode.py)
+  static int div_env = [] {
+    const char* e = getenv("ROTATEK_RING_DIV");
+    return e ? atoi(e) : 6;
+  }();
+  const long long minr_req = (pl.tpu + div_env - 1) / (div_env > 0 ? div_env : 6);
+  long long cmax_ctas = pl.T / (minr_req > 0 ? minr_req : 1);
+  if (cmax_ctas < 1) cmax_ctas = 1;
+  for (pl.C = (int)(cmax_ctas < sms ? cmax_ctas : sms);; --pl.C) {
     const long long minr = pl.T / pl.C;  // >= 1 tile per CTA
     pl.cmax = (int)((pl.tpu + minr - 1) / minr) + 1;
     if (pl.cmax > pl.C) pl.cmax = pl.C;
