@@ -197,6 +197,42 @@ def test_rotation_orthonormal_and_residual_orthogonal():
     np.testing.assert_allclose(dmu_all, 0.0, atol=1e-13)
 
 
+def test_dmu_from_R_invariants():
+    """orc_dmu_from_R (Alg. 1 l.15: delta_mu = mu - R R^T mu for a given, e.g. stored
+    fp32, R) pinned by what the projection must satisfy, not by retyping it:
+      * orthonormal R: delta_mu is orthogonal to range(R) and Pythagoras holds;
+      * mu in range(R) gives 0, mu orthogonal to range(R) gives mu itself;
+      * non-orthonormal stored-fp32 R (what the GPU holds): R^T delta_mu = (I - R^T R) R^T mu,
+        i.e. of the size of R's rounding, and the decomposition R(R^T mu) + delta_mu = mu;
+      * linear in mu, batched per unit (a unit/row mix-up fails the per-unit checks)."""
+    rng = np.random.default_rng(31)
+    U, d, r = 3, 24, 7
+    Q = np.stack([np.linalg.qr(rng.standard_normal((d, d)))[0] for _ in range(U)])
+    R = np.ascontiguousarray(Q[:, :, :r])
+    mu = rng.standard_normal((U, d)) * np.array([1.0, 10.0, 0.1])[:, None]
+    dmu = orc.dmu_from_R(R, mu)
+    for u in range(U):
+        assert np.abs(R[u].T @ dmu[u]).max() <= 1e-13 * np.abs(mu[u]).max() * d
+        proj2 = float(np.sum((R[u].T @ mu[u]) ** 2))
+        assert abs(np.sum(dmu[u] ** 2) - (np.sum(mu[u] ** 2) - proj2)) <= 1e-12 * np.sum(mu[u] ** 2)
+    inside = np.einsum("udr,ur->ud", R, rng.standard_normal((U, r)))
+    np.testing.assert_allclose(orc.dmu_from_R(R, inside), 0.0, atol=1e-13)
+    outside = np.einsum("udk,uk->ud", Q[:, :, r:], rng.standard_normal((U, d - r)))
+    np.testing.assert_allclose(orc.dmu_from_R(R, outside), outside, atol=1e-13)
+    # stored fp32 R: not exactly orthonormal; the residual's component in range(R) is exactly
+    # (I - R^T R) R^T mu, which is of the order of R's rounding
+    R32 = R.astype(np.float32).astype(np.float64)
+    d32 = orc.dmu_from_R(R32, mu)
+    for u in range(U):
+        got = R32[u].T @ d32[u]
+        want = (np.eye(r) - R32[u].T @ R32[u]) @ (R32[u].T @ mu[u])
+        np.testing.assert_allclose(got, want, atol=1e-12 * np.abs(mu[u]).max())
+        assert np.abs(got).max() <= 1e-6 * np.abs(mu[u]).max()
+    # linearity
+    np.testing.assert_allclose(orc.dmu_from_R(R32, 3.0 * mu - 2.0 * inside),
+                               3.0 * d32 - 2.0 * orc.dmu_from_R(R32, inside), atol=1e-12 * np.abs(mu).max())
+
+
 def test_eckart_young_brute_force():
     """Captured variance tr(R_r^T C_q R_r) = sum of the top-r eigenvalues and is
     >= the variance of every coordinate subset of size r (the `\\iffalse`
