@@ -52,7 +52,7 @@
 extern "C" {
 #endif
 
-#define ROTATEK_ABI_VERSION 2
+#define ROTATEK_ABI_VERSION 3
 
 typedef struct CUstream_st* rotatek_stream_t; /* == cudaStream_t; NULL = legacy default */
 
@@ -184,6 +184,42 @@ rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dims, const void* K, c
 rotatek_status rotatek_compress_kv_ex2(const rotatek_dims* dims, int32_t r_units, const void* K,
                                        const float* R, void* K_comp, uint32_t flags,
                                        rotatek_stream_t stream);
+
+/*
+ * Token selection fused into the prefill (NEXT-2; PAPER.md P:133-135 fig:inference_flow
+ * "following visual token compression", P:597 FastV K = 2 / VisionZip survivors; reading
+ * Q20: the rotation is calibrated on the surviving visual tokens only).
+ * Logical visual tokens of unit u: t = 0 .. n_u - 1, where
+ *   n_u = n_vis_u ? clamp(n_vis_u[u], 0, dims->n_vis) : dims->n_vis
+ * (n_vis_u: [U] int32 device, a padded batch of requests with different image-token counts),
+ * and token t's key row is
+ *   K[u][tok_idx[u * n_vis + t]]   with K [U, n_src, d]        if tok_idx != NULL
+ *                                  (tok_idx [U, n_vis] int32 device: the survivors' positions
+ *                                   in the unpruned cache, e.g. ascending FastV indices),
+ *   K[u][t]                        with K [U, n_vis, d]        otherwise.
+ * The kernels gather those rows while loading (the producer warp's cp.async copies write the
+ * swizzled tile the tensor cores read): no compacted copy of K is made.  Rows past n_u, and
+ * out-of-range indices, read as zero keys and are never loaded.
+ *
+ * rotatek_calibrate_tokens: rotatek_calibrate (Alg. 1) over the n_u logical tokens of each unit
+ *   (mu = column sum / n_u, C = S - n_u mu mu^T).  n_u must be >= 1 per unit (a unit with no
+ *   token has an undefined rotation).
+ * rotatek_compress_kv_tokens: K_comp [U, n_vis, r] with K_comp[u][t] = RNE(K_row(t) R_u) for
+ *   t < n_u and exactly 0 for n_u <= t < n_vis (decode with rotatek_decode_attn_varlen and the
+ *   same n_vis_u reads only the first n_u rows).
+ * Both need the tensor-core path (bf16, d = 128; else ROTATEK_ERR_UNSUPPORTED), 16-byte aligned
+ * token arrays (ROTATEK_ERR_ALIGN) and n_src >= 1 with a token list (ROTATEK_ERR_DIMS); other
+ * arguments and errors as rotatek_calibrate / rotatek_compress_kv_ex2.
+ */
+rotatek_status rotatek_calibrate_tokens(const rotatek_dims* dims, uint32_t flags, const void* K,
+                                        int32_t n_src, const int32_t* tok_idx, const int32_t* n_vis_u,
+                                        const void* Qw, float* R, float* dmu, float* eigvals,
+                                        uint32_t* keep_mask, int32_t* keep_idx, float* R_full,
+                                        int32_t* info, void* workspace, size_t workspace_bytes,
+                                        rotatek_stream_t stream);
+rotatek_status rotatek_compress_kv_tokens(const rotatek_dims* dims, int32_t r_units, const void* K,
+                                         int32_t n_src, const int32_t* tok_idx, const int32_t* n_vis_u,
+                                         const float* R, void* K_comp, rotatek_stream_t stream);
 
 /*
  * Alg. 2 for all U*G query heads in one launch:

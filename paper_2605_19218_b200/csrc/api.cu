@@ -85,12 +85,12 @@ size_t rotatek_workspace_bytes(const rotatek_dims* dm, rotatek_op op) {
   return 0;
 }
 
-rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const void* K,
-                                 const void* Qw, float* R, float* dmu, float* eigvals,
-                                 uint32_t* keep_mask, int32_t* keep_idx, float* R_full,
-                                 int32_t* info, void* workspace, size_t workspace_bytes,
-                                 rotatek_stream_t stream) {
-  begin_call();
+namespace {
+// rotatek_calibrate / rotatek_calibrate_tokens (tsrc: token list or per-unit lengths)
+rotatek_status calibrate_impl(const rotatek_dims* dm, uint32_t flags, const void* K, const rk::TokSrc& tsrc,
+                              const void* Qw, float* R, float* dmu, float* eigvals, uint32_t* keep_mask,
+                              int32_t* keep_idx, float* R_full, int32_t* info, void* workspace,
+                              size_t workspace_bytes, rotatek_stream_t stream) {
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   const int U = dm->units, G = dm->group, d = dm->head_dim, r = dm->rank, N = dm->n_vis,
@@ -112,17 +112,48 @@ rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const v
   int n = 0;
   if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
   const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::cov_tc_supported(d, bf16);
-  if ((s = launched(tc ? rk::launch_cov_tc(U, N, center, K, ws, st) : rk::launch_cov(U, N, d, bf16, K, ws, st),
+  if (tsrc.active() && !tc)
+    return fail(ROTATEK_ERR_UNSUPPORTED, "token lists / per-unit lengths need the tensor-core path (bf16, d = 128)");
+  if ((s = launched(tc ? rk::launch_cov_tc(U, N, center, K, ws, st, true, tsrc)
+                       : rk::launch_cov(U, N, d, bf16, K, ws, st),
                     &n)))
     return s;
   if (!(tc && ws.parts == 1))  // the tensor-core kernel finalizes in place when one CTA sees the unit
-    if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st), &n))) return s;
+    if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st, tsrc.nvu), &n))) return s;
   if ((s = launched(rk::launch_jacobi(U, d, fp64, ws, st), &n))) return s;
   if ((s = launched(rk::launch_select_gather(U, d, r, /*fp64_vecs=*/true, bf16, center, ws, R, dmu, eigvals,
                                              keep_mask, keep_idx, R_full, info, st), &n)))
     return s;
   g_launches = n;
   return ROTATEK_OK;
+}
+}  // namespace
+
+rotatek_status rotatek_calibrate(const rotatek_dims* dm, uint32_t flags, const void* K,
+                                 const void* Qw, float* R, float* dmu, float* eigvals,
+                                 uint32_t* keep_mask, int32_t* keep_idx, float* R_full,
+                                 int32_t* info, void* workspace, size_t workspace_bytes,
+                                 rotatek_stream_t stream) {
+  begin_call();
+  return calibrate_impl(dm, flags, K, rk::TokSrc(), Qw, R, dmu, eigvals, keep_mask, keep_idx, R_full, info,
+                        workspace, workspace_bytes, stream);
+}
+
+rotatek_status rotatek_calibrate_tokens(const rotatek_dims* dm, uint32_t flags, const void* K, int32_t n_src,
+                                        const int32_t* tok_idx, const int32_t* n_vis_u, const void* Qw,
+                                        float* R, float* dmu, float* eigvals, uint32_t* keep_mask,
+                                        int32_t* keep_idx, float* R_full, int32_t* info, void* workspace,
+                                        size_t workspace_bytes, rotatek_stream_t stream) {
+  begin_call();
+  if ((tok_idx && !aligned16(tok_idx)) || (n_vis_u && !aligned16(n_vis_u)))
+    return fail(ROTATEK_ERR_ALIGN, "token arrays not 16-byte aligned");
+  if (tok_idx && n_src < 1) return fail(ROTATEK_ERR_DIMS, "n_src must be >= 1 with a token list");
+  rk::TokSrc tsrc;
+  tsrc.idx = tok_idx;
+  tsrc.nvu = n_vis_u;
+  tsrc.n_src = tok_idx ? n_src : (dm ? dm->n_vis : 0);
+  return calibrate_impl(dm, flags, K, tsrc, Qw, R, dmu, eigvals, keep_mask, keep_idx, R_full, info,
+                        workspace, workspace_bytes, stream);
 }
 
 rotatek_status rotatek_calibrate_subspace(const rotatek_dims* dm, uint32_t flags, const void* K,
@@ -228,9 +259,9 @@ rotatek_status rotatek_calibrate_from_state(const rotatek_dims* dm, uint32_t fla
   return ROTATEK_OK;
 }
 
-rotatek_status rotatek_compress_kv_ex2(const rotatek_dims* dm, int32_t r_units, const void* K, const float* R,
-                                      void* K_comp, uint32_t flags, rotatek_stream_t stream) {
-  begin_call();
+namespace {
+rotatek_status compress_impl(const rotatek_dims* dm, int32_t r_units, const void* K, const rk::TokSrc& tsrc,
+                             const float* R, void* K_comp, uint32_t flags, rotatek_stream_t stream) {
   rotatek_status s = check_dims(dm);
   if (s != ROTATEK_OK) return s;
   if (!K || !R || !K_comp) return fail(ROTATEK_ERR_NULL, "K, R and K_comp are required");
@@ -241,16 +272,39 @@ rotatek_status rotatek_compress_kv_ex2(const rotatek_dims* dm, int32_t r_units, 
     return fail(ROTATEK_ERR_DIMS, "r_units must divide units (0: one rotation per unit)");
   const bool bf16 = dm->dtype == ROTATEK_BF16;
   const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::compress_tc_supported(d, r, bf16);
+  if (tsrc.active() && !tc)
+    return fail(ROTATEK_ERR_UNSUPPORTED, "token lists / per-unit lengths need the tensor-core path (bf16, d = 128)");
   if (!tc && ((size_t)d * r + 64 * (size_t)d) * 4 > 227 * 1024)
     return fail(ROTATEK_ERR_UNSUPPORTED, "compress: d*r too large");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int n = 0;
-  if ((s = launched(tc ? rk::launch_compress_tc(dm->units, dm->n_vis, r, K, R, K_comp, st, r_units)
+  if ((s = launched(tc ? rk::launch_compress_tc(dm->units, dm->n_vis, r, K, R, K_comp, st, r_units, tsrc)
                        : rk::launch_compress(dm->units, dm->n_vis, d, r, bf16, K, R, K_comp, st, r_units),
                     &n)))
     return s;
   g_launches = n;
   return ROTATEK_OK;
+}
+}  // namespace
+
+rotatek_status rotatek_compress_kv_ex2(const rotatek_dims* dm, int32_t r_units, const void* K, const float* R,
+                                      void* K_comp, uint32_t flags, rotatek_stream_t stream) {
+  begin_call();
+  return compress_impl(dm, r_units, K, rk::TokSrc(), R, K_comp, flags, stream);
+}
+
+rotatek_status rotatek_compress_kv_tokens(const rotatek_dims* dm, int32_t r_units, const void* K, int32_t n_src,
+                                         const int32_t* tok_idx, const int32_t* n_vis_u, const float* R,
+                                         void* K_comp, rotatek_stream_t stream) {
+  begin_call();
+  if ((tok_idx && !aligned16(tok_idx)) || (n_vis_u && !aligned16(n_vis_u)))
+    return fail(ROTATEK_ERR_ALIGN, "token arrays not 16-byte aligned");
+  if (tok_idx && n_src < 1) return fail(ROTATEK_ERR_DIMS, "n_src must be >= 1 with a token list");
+  rk::TokSrc tsrc;
+  tsrc.idx = tok_idx;
+  tsrc.nvu = n_vis_u;
+  tsrc.n_src = tok_idx ? n_src : (dm ? dm->n_vis : 0);
+  return compress_impl(dm, r_units, K, tsrc, R, K_comp, 0u, stream);
 }
 
 rotatek_status rotatek_compress_kv_ex(const rotatek_dims* dm, const void* K, const float* R,

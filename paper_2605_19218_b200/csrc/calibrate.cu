@@ -156,14 +156,19 @@ __global__ void __launch_bounds__(256) finalize_kernel(int N, int d, int parts, 
                                                        const double* __restrict__ colpart,
                                                        const double* __restrict__ sigma,
                                                        double* __restrict__ cq,
-                                                       double* __restrict__ mu_out) {
+                                                       double* __restrict__ mu_out,
+                                                       const int32_t* __restrict__ nvu) {
   extern __shared__ double sh_mu[];  // [d] mu, [d] sigma
   double* sh_sig = sh_mu + d;
   const int u = blockIdx.x;
+  if (nvu != nullptr) {  // per-unit token counts (NEXT-2): mu and C over the unit's own tokens
+    const int v = nvu[u];
+    N = v < 0 ? 0 : (v < N ? v : N);
+  }
   for (int j = threadIdx.x; j < d; j += blockDim.x) {
     double s = 0.0;
     for (int p = 0; p < parts; ++p) s += colpart[((size_t)u * parts + p) * d + j];
-    double m = center ? s / (double)N : 0.0;
+    double m = (center && N > 0) ? s / (double)N : 0.0;
     sh_mu[j] = m;
     if (blockIdx.y == 0) mu_out[(size_t)u * d + j] = m;
     sh_sig[j] = sigma[(size_t)u * d + j];
@@ -182,9 +187,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(int N, int d, int parts, 
   }
 }
 
-int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st) {
+int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st, const int32_t* nvu) {
   finalize_kernel<<<dim3(U, 16), 256, 2 * d * sizeof(double), st>>>(N, d, ws.parts, center, ws.covpart,
-                                                          ws.colpart, ws.sigma, ws.cq, ws.mu);
+                                                          ws.colpart, ws.sigma, ws.cq, ws.mu, nvu);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -12,6 +12,7 @@
 // Work item = (unit, token part); a CTA streams its part through a 3-stage TMA ring with
 // double-buffered TMEM accumulators.  Tokens past N are zero-filled by TMA and not stored.
 #include <cstdio>
+#include <cstring>
 
 #include "internal.h"
 #include "tc_common.cuh"
@@ -46,7 +47,8 @@ __device__ __forceinline__ uint16_t bf16_bits_rn(float x) {
 template <int RK>
 __global__ void __launch_bounds__(kThreads, 2) compress_tc_kernel(const __grid_constant__ CUtensorMap tmap, int N,
                                                                   int parts, const float* __restrict__ R,
-                                                                  __nv_bfloat16* __restrict__ Kc, int nR) {
+                                                                  __nv_bfloat16* __restrict__ Kc, int nR,
+                                                                  TokSrc tsrc, const __nv_bfloat16* __restrict__ Kg) {
   using C = CmpCfg<RK>;
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
@@ -80,9 +82,10 @@ __global__ void __launch_bounds__(kThreads, 2) compress_tc_kernel(const __grid_c
     *reinterpret_cast<__nv_bfloat16*>(Bsm + 1 * C::B_SPLIT + off) = m;
     *reinterpret_cast<__nv_bfloat16*>(Bsm + 2 * C::B_SPLIT + off) = l;
   }
+  const bool gathered = tsrc.active();  // token list / per-unit lengths: cp.async producer
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], gathered ? 32 : 1);
       mbar_init(&empty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -90,7 +93,7 @@ __global__ void __launch_bounds__(kThreads, 2) compress_tc_kernel(const __grid_c
       mbar_init(&tempty[a], 4);
     }
     fence_mbar_init();
-    tc::prefetch_tmap(&tmap);
+    if (!gathered) tc::prefetch_tmap(&tmap);
   }
   if (warp == 1) tc::tmem_alloc(tmem_slot, C::TMEM_COLS);
   fence_proxy_async();  // generic-proxy writes of B must be visible to the tensor core (async proxy)
@@ -99,7 +102,18 @@ __global__ void __launch_bounds__(kThreads, 2) compress_tc_kernel(const __grid_c
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 && gathered) {
+    // all 32 lanes gather the tile's rows (tok_gather.cuh); rows past the unit's count are
+    // zero-filled, so their K~ rows come out exactly 0
+    const int nv = tsrc.valid(u, N);
+    for (int i = 0; i < nt; ++i) {
+      const int s = i % kStages;
+      mbar_wait(&empty[s], ((i / kStages) & 1) ^ 1);
+      gather_tile_128x128(tsrc, Kg, u, N, nv, (t_lo + i) * kTM, sm + s * kStageBytes, kHalf, lane);
+      cp_async_arrive_noinc(&full[s]);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       for (int i = 0; i < nt; ++i) {
@@ -119,6 +133,7 @@ __global__ void __launch_bounds__(kThreads, 2) compress_tc_kernel(const __grid_c
       for (int i = 0; i < nt; ++i) {
         const int s = i % kStages, a = i & 1;
         mbar_wait(&full[s], (i / kStages) & 1);
+        if (gathered) fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core
         mbar_wait(&tempty[a], ((i >> 1) & 1) ^ 1);
         tc::fence_after();
         const uint32_t abase = smem_u32(sm + s * kStageBytes);
@@ -185,10 +200,11 @@ bool compress_tc_supported(int d, int r, bool bf16) {
 
 template <int RK>
 static int launch_compress_tc_r(int U, int N, const void* K, const float* R, void* Kc, cudaStream_t st,
-                                int nR) {
+                                int nR, const TokSrc& tsrc) {
   using C = CmpCfg<RK>;
   CUtensorMap map;
-  if (!encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTM, 128)) return -2;
+  memset(&map, 0, sizeof(map));
+  if (!tsrc.active() && !encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTM, 128)) return -2;
   static int attr_slot[kMaxDevices];
   once_per_device(attr_slot, [] {
     cudaFuncSetAttribute(compress_tc_kernel<RK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
@@ -200,17 +216,18 @@ static int launch_compress_tc_r(int U, int N, const void* K, const float* R, voi
   if (parts < 1) parts = 1;
   dim3 grid(parts, U);
   compress_tc_kernel<RK><<<grid, kThreads, C::SMEM, st>>>(map, N, parts, R, static_cast<__nv_bfloat16*>(Kc),
-                                                          nR > 0 ? nR : U);
+                                                          nR > 0 ? nR : U, tsrc,
+                                                          static_cast<const __nv_bfloat16*>(K));
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
 int launch_compress_tc(int U, int N, int r, const void* K, const float* R, void* Kc, cudaStream_t st,
-                       int nR) {
+                       int nR, const TokSrc& tsrc) {
   switch (r) {
-    case 16: return launch_compress_tc_r<16>(U, N, K, R, Kc, st, nR);
-    case 32: return launch_compress_tc_r<32>(U, N, K, R, Kc, st, nR);
-    case 64: return launch_compress_tc_r<64>(U, N, K, R, Kc, st, nR);
-    case 128: return launch_compress_tc_r<128>(U, N, K, R, Kc, st, nR);
+    case 16: return launch_compress_tc_r<16>(U, N, K, R, Kc, st, nR, tsrc);
+    case 32: return launch_compress_tc_r<32>(U, N, K, R, Kc, st, nR, tsrc);
+    case 64: return launch_compress_tc_r<64>(U, N, K, R, Kc, st, nR, tsrc);
+    case 128: return launch_compress_tc_r<128>(U, N, K, R, Kc, st, nR, tsrc);
   }
   return -2;
 }

@@ -18,9 +18,11 @@
 // Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
 // warps 2..9 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4).
 #include <cstdio>
+#include <cstring>
 
 #include "internal.h"
 #include "tc_common.cuh"
+#include "tok_gather.cuh"
 
 namespace rk {
 
@@ -42,7 +44,8 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
                                                              double* __restrict__ colpart,
                                                              const double* __restrict__ sigma,
                                                              double* __restrict__ cq, double* __restrict__ mu,
-                                                             bool center, bool fused) {
+                                                             bool center, bool fused, TokSrc tsrc,
+                                                             const __nv_bfloat16* __restrict__ Kg) {
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
   unsigned char* ones = sm + kStages * kStageBytes;  // 1024-aligned
@@ -66,9 +69,10 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     nch = (int)((long long)nchunks_all * (p + 1) / parts) - c_lo;
   };
 
+  const bool gathered = tsrc.active();  // token list / per-unit lengths: cp.async producer
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], gathered ? 32 : 1);
       mbar_init(&empty[s], 1);  // released by the MMA commit alone (no smem column-sum pass)
     }
     for (int a = 0; a < 2; ++a) {
@@ -89,7 +93,22 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
   tc::fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 && gathered) {
+    // all 32 lanes gather the chunk's rows (tok_gather.cuh); zero rows past the unit's count
+    int gi = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+      int u, p, c_lo, nch;
+      item_range(it, u, p, c_lo, nch);
+      const int nv = tsrc.valid(u, N);
+      for (int i = 0; i < nch; ++i, ++gi) {
+        const int s = gi % kStages;
+        mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
+        gather_tile_128x128(tsrc, Kg, u, N, nv, (c_lo + i) * kTK, sm + s * kStageBytes, kHalfBytes, lane);
+        cp_async_arrive_noinc(&full[s]);
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else if (warp == 0) {
     if (lane == 0) {
       const uint64_t pol = policy_evict_first();
       int gi = 0;  // running chunk counter (ring stage / phase)
@@ -123,6 +142,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
           const int s = gi % kStages, a = gw & 1;
           const bool first = (i % kWin) == 0, last = (i % kWin) == kWin - 1 || i == nch - 1;
           mbar_wait(&full[s], (gi / kStages) & 1);
+          if (gathered) fence_proxy_async();  // cp.async (generic proxy) writes -> tensor core
           if (first) mbar_wait(&tempty[a], ((gw >> 1) & 1) ^ 1);
           tc::fence_after();
           const uint32_t base = smem_u32(sm + s * kStageBytes);
@@ -191,19 +211,20 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     if (fused) {
       // parts == 1: this CTA saw every token of the unit -> finalize here (mu, C, C_q)
       const double* sg = sigma + (size_t)u * kDc;
-      const double mur = center ? colsum_sm[row] / (double)N : 0.0;
+      const double nu = (double)tsrc.valid(u, N);  // tokens of the unit (per-unit lengths)
+      const double mur = center ? colsum_sm[row] / nu : 0.0;
       const double sr = sg[row];
       double* cqr = cq + (size_t)u * kDc * kDc + (size_t)row * kDc + h * 64;
 #pragma unroll
       for (int j = 0; j < 64; j += 2) {
         const int c0 = h * 64 + j;
-        const double m0 = center ? colsum_sm[c0] / (double)N : 0.0;
-        const double m1 = center ? colsum_sm[c0 + 1] / (double)N : 0.0;
-        const double v0 = sr * sg[c0] * (acc[j] - (double)N * mur * m0);
-        const double v1 = sr * sg[c0 + 1] * (acc[j + 1] - (double)N * mur * m1);
+        const double m0 = center ? colsum_sm[c0] / nu : 0.0;
+        const double m1 = center ? colsum_sm[c0 + 1] / nu : 0.0;
+        const double v0 = sr * sg[c0] * (acc[j] - nu * mur * m0);
+        const double v1 = sr * sg[c0 + 1] * (acc[j + 1] - nu * mur * m1);
         *reinterpret_cast<double2*>(cqr + j) = make_double2(v0, v1);
       }
-      if (et < kDc) mu[(size_t)u * kDc + et] = center ? colsum_sm[et] / (double)N : 0.0;
+      if (et < kDc) mu[(size_t)u * kDc + et] = center ? colsum_sm[et] / nu : 0.0;
     } else {
       double* out = covpart + ((size_t)u * parts + p) * kDc * kDc + (size_t)row * kDc + h * 64;
 #pragma unroll
@@ -266,9 +287,10 @@ bool encode_tmap_3d_bf16_strided(CUtensorMap* map, const void* base, uint64_t d0
 bool cov_tc_supported(int d, bool bf16) { return bf16 && d == kDc && get_encode() != nullptr; }
 
 int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, cudaStream_t st,
-                  bool allow_fused) {
+                  bool allow_fused, const TokSrc& tsrc) {
   CUtensorMap map;
-  if (!encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTK, 128)) return -2;
+  memset(&map, 0, sizeof(map));
+  if (!tsrc.active() && !encode_tmap_3d_bf16(&map, K, kDc, (uint64_t)N, (uint64_t)U, 64, kTK, 128)) return -2;
   static int attr_slot[kMaxDevices];
   once_per_device(attr_slot, [] {
     cudaFuncSetAttribute(cov_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem);
@@ -279,7 +301,8 @@ int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, c
   const int grid = nitems < kNumSMs ? nitems : kNumSMs;
   // parts == 1: the kernel also finalizes (mu, C = S - N mu mu^T, C_q) -- no finalize launch
   cov_tc_kernel<<<grid, kThreads, kSmem, st>>>(map, N, U, ws.parts, ws.covpart, ws.colpart, ws.sigma, ws.cq,
-                                               ws.mu, center, allow_fused && ws.parts == 1);
+                                               ws.mu, center, allow_fused && ws.parts == 1, tsrc,
+                                               static_cast<const __nv_bfloat16*>(K));
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 

@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include "tok_gather.cuh"
+
 namespace rk {
 
 constexpr int kNumSMs = 148;
@@ -61,16 +63,17 @@ int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws,
 bool cov_tc_supported(int d, bool bf16);
 bool compress_tc_supported(int d, int r, bool bf16);
 int launch_compress_tc(int U, int N, int r, const void* K, const float* R, void* Kc, cudaStream_t st,
-                       int nR = 0);
+                       int nR = 0, const TokSrc& tsrc = TokSrc());
 // parts == 1 also finalizes (writes cq and mu): the caller skips launch_finalize
 int launch_cov_tc(int U, int N, bool center, const void* K, const CalibWs& ws, cudaStream_t st,
-                  bool allow_fused = true);
+                  bool allow_fused = true, const TokSrc& tsrc = TokSrc());
 // calibration statistics state (rotatek_calib_accumulate / rotatek_calibrate_from_state)
 int launch_state_accumulate(int U, int N, int d, int nS, bool weight, const CalibWs& ws, double* state,
                             cudaStream_t st);
 int launch_state_finalize(int nS, int d, bool center, bool weight, const double* state, const CalibWs& ws,
                           cudaStream_t st);
-int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st);
+int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st,
+                    const int32_t* nvu = nullptr);
 int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st);
 int launch_select_gather(int U, int d, int r, bool fp64_vecs, bool bf16x2, bool center,
                          const CalibWs& ws, float* R, float* dmu, float* eigvals,

@@ -44,7 +44,7 @@ def test_exports_every_declared_symbol(rk):
 
 def test_version_and_strings(rk):
     L = rk.lib()
-    assert L.rotatek_abi_version() == 2  # 2: rotatek_dims.text_stride
+    assert L.rotatek_abi_version() == 3  # 2: rotatek_dims.text_stride; 3: token-list prefill, decode kernel 5
     for code in range(7):
         assert L.rotatek_status_string(code).decode().startswith("ROTATEK_")
 

@@ -10,7 +10,7 @@ for cfg in ${CFGS:-llava_b32 qwen_b32_r32 joint_b64 long_b16}; do
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/launches_${cfg}_${tag}.csv \
     python bench.py --config $cfg --steps 1 --warmup 1 --skip-e2e --skip-cpu --no-graph --layers 2 > /dev/null 2>&1
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"decode_(fast|gqa)" -s 2 -c 1 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"decode_(fast|gqa|ring)" -s 2 -c 1 \
     -o gpurun_out/prof_decode_${cfg}_${tag} -f \
     python bench.py --config $cfg --steps 1 --warmup 1 --skip-full --skip-e2e --skip-cpu --no-graph --layers 1 > gpurun_out/ncu_${cfg}_${tag}.log 2>&1
   ncu -i gpurun_out/prof_decode_${cfg}_${tag}.ncu-rep --page details --csv > gpurun_out/ncu_decode_${cfg}_${tag}_details.csv 2>/dev/null

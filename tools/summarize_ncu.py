@@ -1,8 +1,12 @@
 #!/usr/bin/env python
-"""Summarise ncu captures from tools/profile_all.sh into profiles/ (tag given as argv[1]).
+"""Summarise ncu captures from tools/profile_all.sh (markdown tables on stdout).
 
-Writes profiles/ncu_traffic.json (dram bytes per decode launch, read by bench.py for
-roofline.traffic) and prints a markdown table of the key metrics per kernel."""
+    python tools/summarize_ncu.py --tag r2a [--src gpurun_out] [--write-traffic]
+
+--write-traffic MERGES the decode captures found for the tag into profiles/ncu_traffic.json
+(dram bytes per decode launch, read by bench.py for roofline.traffic); configs without a
+capture keep their entries.  Without it nothing is written."""
+import argparse
 import csv
 import json
 import os
@@ -13,14 +17,19 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 from workload import CONFIGS, decode_bytes  # noqa: E402
 
-tag = sys.argv[1] if len(sys.argv) > 1 else "r1b"
-src = sys.argv[2] if len(sys.argv) > 2 else os.path.join(ROOT, "gpurun_out")
+ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+ap.add_argument("--tag", required=True, help="capture tag, e.g. r2a (file names *_<tag>_raw.csv)")
+ap.add_argument("--src", default=os.path.join(ROOT, "gpurun_out"))
+ap.add_argument("--write-traffic", action="store_true", help="merge into profiles/ncu_traffic.json")
+opt = ap.parse_args()
+tag, src = opt.tag, opt.src
 
 WANT = {
     "gpu__time_duration.sum": "time",
     "dram__bytes_read.sum": "dram_read",
     "dram__bytes_write.sum": "dram_write",
-    "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed": "dram_pct",
+    "dram__bytes_read.sum.pct_of_peak_sustained_elapsed": "dram_read_pct",
+    "dram__bytes_write.sum.pct_of_peak_sustained_elapsed": "dram_write_pct",
     "dram__bytes.sum.per_second": "dram_bps",
     "sm__ops_path_tensor_op_utchmma_src_bf16_dst_fp32_sparsity_off.avg.pct_of_peak_sustained_elapsed": "utc_pct",
     "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed": "tensor_pct",
@@ -67,12 +76,15 @@ def raw_rows(path):
                 elif k.startswith("dram__bytes") and u == "Kbyte":
                     x *= 1e3
                 rec[v] = x
+        rec["dram_pct"] = rec.get("dram_read_pct", 0.0) + rec.get("dram_write_pct", 0.0)
         out.append(rec)
     return out
 
 
-traffic = {"_source": f"ncu --set full --clock-control none (tools/profile_all.sh, tag {tag}), one decode "
-                      "launch, dram__bytes_read.sum + dram__bytes_write.sum"}
+tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+traffic = json.load(open(tpath)) if os.path.exists(tpath) else {}
+traffic["_source"] = ("ncu --set full --clock-control none (tools/profile_all.sh), one decode launch, "
+                      "dram__bytes_read.sum + dram__bytes_write.sum; per-config 'capture' names the file")
 lines = ["| config | kernel | ncu time (us) | dram read+write (MB) | alg. bytes (MB) | traffic/alg | "
          "DRAM % peak | SM issue % | regs |", "|---|---|---|---|---|---|---|---|---|"]
 for cfg in ("llava_b32", "qwen_b32_r32", "joint_b64", "long_b16"):
@@ -91,7 +103,8 @@ for cfg in ("llava_b32", "qwen_b32_r32", "joint_b64", "long_b16"):
     lines.append(f"| {cfg} | {r['kernel'][:40]} | {r.get('time', 0) / 1e3:.1f} | {tot / 1e6:.1f} | "
                  f"{alg / 1e6:.1f} | {tot / alg:.3f} | {r.get('dram_pct', 0):.1f} | "
                  f"{r.get('sm_issue_pct', r.get('issue_pct', 0)):.1f} | {int(r.get('regs', 0))} |")
-json.dump(traffic, open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
+if opt.write_traffic:
+    json.dump(traffic, open(tpath, "w"), indent=1)
 print("\n".join(lines))
 
 p = os.path.join(src, f"ncu_prefill_llava_b32_{tag}_raw.csv")
