@@ -110,10 +110,10 @@ rotatek_status calibrate_impl(const rotatek_dims* dm, uint32_t flags, const void
   if (!workspace || workspace_bytes < need) return fail(ROTATEK_ERR_WORKSPACE, "workspace too small");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int n = 0;
-  if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
   const bool tc = !(flags & ROTATEK_SIMT_ONLY) && rk::cov_tc_supported(d, bf16);
   if (tsrc.active() && !tc)
     return fail(ROTATEK_ERR_UNSUPPORTED, "token lists / per-unit lengths need the tensor-core path (bf16, d = 128)");
+  if ((s = launched(rk::launch_sigma(U, G, W, d, bf16, weight, Qw, ws.sigma, st), &n))) return s;
   if ((s = launched(tc ? rk::launch_cov_tc(U, N, center, K, ws, st, true, tsrc)
                        : rk::launch_cov(U, N, d, bf16, K, ws, st),
                     &n)))

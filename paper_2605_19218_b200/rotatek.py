@@ -81,13 +81,17 @@ def lib():
             L.rotatek_calibrate_from_state.argtypes = [dp, u32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                                        sz, vp]
             L.rotatek_merge_partials.argtypes = [i32, i32, i32, i32, vp, vp, vp]
+            L.rotatek_calibrate_tokens.argtypes = [dp, u32, vp, i32, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                                   vp, vp, sz, vp]
+            L.rotatek_compress_kv_tokens.argtypes = [dp, i32, vp, i32, vp, vp, vp, vp, vp]
             L.rotatek_gather_tokens.argtypes = [i32, i32, i32, i32, vp, vp, vp, vp, vp]
             for fn in ("rotatek_calibrate", "rotatek_compress_kv", "rotatek_compress_kv_ex",
                        "rotatek_decode_attn",
                        "rotatek_decode_attn_ex", "rotatek_select_topr", "rotatek_decode_attn_partial",
                        "rotatek_merge_partials", "rotatek_decode_attn_ex2", "rotatek_compress_kv_ex2",
                        "rotatek_calib_accumulate", "rotatek_calibrate_from_state",
-                       "rotatek_gather_tokens", "rotatek_decode_attn_varlen"):
+                       "rotatek_gather_tokens", "rotatek_decode_attn_varlen",
+                       "rotatek_calibrate_tokens", "rotatek_compress_kv_tokens"):
                 getattr(L, fn).restype = ctypes.c_int
             L.rotatek_status_string.argtypes = [ctypes.c_int]
             L.rotatek_status_string.restype = ctypes.c_char_p
@@ -192,13 +196,30 @@ def workspace(dims: Dims, op: int, device, stream=None) -> torch.Tensor:
 
 
 # --------------------------------------------------------------------------- calibrate
+def _tok_args(K, tok_idx, n_vis_u, n_log):
+    """Checks of the token-selection inputs (include/rotatek.h, rotatek_calibrate_tokens)."""
+    U = K.shape[0]
+    if tok_idx is not None:
+        assert tok_idx.dtype == torch.int32 and tok_idx.shape == (U, n_log) and tok_idx.is_cuda
+    if n_vis_u is not None:
+        assert n_vis_u.dtype == torch.int32 and n_vis_u.shape == (U,) and n_vis_u.is_cuda
+
+
 def calibrate(K: torch.Tensor, Qw: torch.Tensor | None, rank: int, flags: int = DEFAULT_FLAGS,
-              *, want_full: bool = False, ws: torch.Tensor | None = None, stream=None) -> dict:
+              *, want_full: bool = False, tok_idx: torch.Tensor | None = None,
+              n_vis_u: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> dict:
     """Alg. 1 steps 1-5 (+ select, delta_mu).  K [U, N, d]; Qw [U, G, W, d] or None.
+    tok_idx [U, n] int32: calibrate on rows tok_idx[u] of K [U, n_src, d] (token pruning
+    survivors, gathered by the kernel); n_vis_u [U] int32: per-unit valid token counts
+    (rotatek_calibrate_tokens).
 
     Returns dict(R [U,d,r] f32, dmu [U,d] f32, eigvals [U,d] f32, mask [U,ceil(d/32)] i32
     (uint32 bit pattern), idx [U,r] i32, info [U] i32, R_full [U,d,d] f32 if want_full)."""
     U, N, d = K.shape
+    n_src = N
+    if tok_idx is not None:
+        N = tok_idx.shape[1]
+    _tok_args(K, tok_idx, n_vis_u, N)
     if Qw is None:
         G, W = 1, 0
     else:
@@ -217,11 +238,18 @@ def calibrate(K: torch.Tensor, Qw: torch.Tensor | None, rank: int, flags: int = 
     out["R_full"] = torch.empty((U, d, d), dtype=torch.float32, device=dev) if want_full else None
     if ws is None:
         ws = workspace(dims, OP_CALIBRATE, dev, stream)
-    _check(lib().rotatek_calibrate(ctypes.byref(dims), flags, _ptr(K),
-                                   _ptr(Qw) if W > 0 else None, _ptr(out["R"]), _ptr(out["dmu"]),
-                                   _ptr(out["eigvals"]), _ptr(out["mask"]), _ptr(out["idx"]),
-                                   _ptr(out["R_full"]), _ptr(out["info"]), _ptr(ws), ws.numel(),
-                                   _stream(stream)))
+    if tok_idx is None and n_vis_u is None:
+        _check(lib().rotatek_calibrate(ctypes.byref(dims), flags, _ptr(K),
+                                       _ptr(Qw) if W > 0 else None, _ptr(out["R"]), _ptr(out["dmu"]),
+                                       _ptr(out["eigvals"]), _ptr(out["mask"]), _ptr(out["idx"]),
+                                       _ptr(out["R_full"]), _ptr(out["info"]), _ptr(ws), ws.numel(),
+                                       _stream(stream)))
+    else:
+        _check(lib().rotatek_calibrate_tokens(ctypes.byref(dims), flags, _ptr(K), n_src, _ptr(tok_idx),
+                                              _ptr(n_vis_u), _ptr(Qw) if W > 0 else None, _ptr(out["R"]),
+                                              _ptr(out["dmu"]), _ptr(out["eigvals"]), _ptr(out["mask"]),
+                                              _ptr(out["idx"]), _ptr(out["R_full"]), _ptr(out["info"]),
+                                              _ptr(ws), ws.numel(), _stream(stream)))
     return out
 
 
@@ -312,10 +340,28 @@ def calibrate_from_state(state: torch.Tensor, rank: int, flags: int = DEFAULT_FL
 
 # --------------------------------------------------------------------------- compress
 def compress_kv(K: torch.Tensor, R: torch.Tensor, out: torch.Tensor | None = None,
-                stream=None, flags: int = 0) -> torch.Tensor:
+                stream=None, flags: int = 0, *, tok_idx: torch.Tensor | None = None,
+                n_vis_u: torch.Tensor | None = None) -> torch.Tensor:
     """Alg. 1 line 14: K~ = RNE(K R_r).  K [U, N, d], R [U, d, r] f32 -> [U, N, r] K.dtype.
-    flags: SIMT_ONLY selects the CUDA-core kernel instead of tcgen05."""
+    flags: SIMT_ONLY selects the CUDA-core kernel instead of tcgen05.
+    tok_idx [U, n] int32 / n_vis_u [U] int32: token selection as calibrate() (output
+    [U, n, r], rows past a unit's count exactly 0; rotatek_compress_kv_tokens)."""
     U, N, d = K.shape
+    if tok_idx is not None or n_vis_u is not None:
+        n_src = N
+        if tok_idx is not None:
+            N = tok_idx.shape[1]
+        _tok_args(K, tok_idx, n_vis_u, N)
+        r = R.shape[2]
+        nR = R.shape[0]
+        assert R.shape == (nR, d, r) and U % nR == 0 and R.dtype == torch.float32
+        if out is None:
+            out = torch.empty((U, N, r), dtype=K.dtype, device=K.device)
+        dims = make_dims(U, 1, d, r, N, 0, 0, _dtype_code(K))
+        _check(lib().rotatek_compress_kv_tokens(ctypes.byref(dims), nR if nR != U else 0, _ptr(K), n_src,
+                                                _ptr(tok_idx), _ptr(n_vis_u), _ptr(R), _ptr(out),
+                                                _stream(stream)))
+        return out
     r = R.shape[2]
     nR = R.shape[0]   # nR < U: shared (offline) rotation, unit u uses R[u % nR]
     assert R.shape == (nR, d, r) and U % nR == 0 and R.dtype == torch.float32

@@ -97,7 +97,7 @@ def test_decode_errors(rk):
     assert call(ktext=0) == rk.ERR_NULL                  # M > 0 needs the text segment
     assert call(nws=8) == rk.ERR_WORKSPACE
     assert call(q=0x1008) == rk.ERR_ALIGN
-    assert call(kernel=5) == rk.ERR_DIMS
+    assert call(kernel=6) == rk.ERR_DIMS
 
 
 def test_decode_varlen_errors(rk):
@@ -145,3 +145,32 @@ def test_product_package_does_not_import_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "from oracle" not in src and "import oracle" not in src, f
                 assert "liboracle" not in src and "orc_" not in src, f
+
+
+def test_token_prefill_host_validation(rk):
+    """rotatek_calibrate_tokens / rotatek_compress_kv_tokens: misaligned token arrays, a token
+    list without n_src, and shapes without the tensor-core path fail before any CUDA work."""
+    L = rk.lib()
+    vp = ctypes.c_void_p
+    d = rk.make_dims(4, 1, 128, 32, 300, 0, 32, rk.BF16)
+
+    def cal(dims, n_src=500, idx=0x7000, nvu=None):
+        return L.rotatek_calibrate_tokens(ctypes.byref(dims), rk.DEFAULT_FLAGS, vp(0x1000), n_src, vp(idx),
+                                          vp(nvu), vp(0x2000), vp(0x3000), vp(0x4000), None, None, None,
+                                          None, None, vp(0x5000), 1 << 40, None)
+
+    def cmp(dims, n_src=500, idx=0x7000, nvu=None):
+        return L.rotatek_compress_kv_tokens(ctypes.byref(dims), 0, vp(0x1000), n_src, vp(idx), vp(nvu),
+                                            vp(0x3000), vp(0x6000), None)
+
+    assert cal(d, idx=0x7004) == rk.ERR_ALIGN
+    assert cal(d, idx=None, nvu=0x7008) == rk.ERR_ALIGN
+    assert cal(d, n_src=0) == rk.ERR_DIMS
+    assert cmp(d, idx=0x7004) == rk.ERR_ALIGN
+    assert cmp(d, n_src=0) == rk.ERR_DIMS
+    f32 = rk.make_dims(4, 1, 128, 32, 300, 0, 32, rk.F32)      # no tensor-core path
+    assert cal(f32) == rk.ERR_UNSUPPORTED
+    assert cmp(f32) == rk.ERR_UNSUPPORTED
+    d64 = rk.make_dims(4, 1, 64, 16, 300, 0, 32, rk.BF16)      # d != 128
+    assert cal(d64) == rk.ERR_UNSUPPORTED
+    assert cmp(d64) == rk.ERR_UNSUPPORTED
