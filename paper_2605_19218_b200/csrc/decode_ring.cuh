@@ -69,8 +69,8 @@ struct RingCfg {
   static constexpr int OFF_RD = OFF_RQ + G * kD * 2; // dmu [128] f32 in chunk 0
   static constexpr int CAP = NCH == 1 ? 4 : 2;       // units per CTA range (query table)
   static constexpr int ENT = QEnt<__nv_bfloat16, RK, G>::BYTES;
-  static constexpr int XREC = 18;                    // exchanged floats per lane (16 acc, m, l)
-  static constexpr int XBYTES = 4 * XREC * 32 * 4;   // group exchange [4 quarters][XREC][32]
+  static constexpr int XLD = kD + 8;                 // exchange row stride (floats): half-warp float2 stores conflict-free
+  static constexpr int XBYTES = 4 * 8 * XLD * 4;     // unit-end exchange [4 slots][8 heads][XLD] f32
   static constexpr int RSCR = 8 * G * (RK + 1) * 4;  // rotation partials [8 warps][G][RK + 1]
   static constexpr int UNI = XBYTES > RSCR ? XBYTES : RSCR;
   static constexpr int MLCAP = 288;                  // (slot, head) pairs the flusher's merge holds
@@ -78,18 +78,25 @@ struct RingCfg {
   static constexpr int OFF_TAB = 0;                  // query table [CAP] entries
   static constexpr int OFF_X = OFF_TAB + CAP * ENT;  // exchange / rotation scratch (union)
   static constexpr int OFF_ML = OFF_X + UNI;         // flusher (m, l) table [MLCAP][2] f32
-  static constexpr int OFF_P = OFF_ML + MLCAP * 8;   // P fragments [2 groups][8 n-blocks][2][32] u32
-  static constexpr int OFF_MX = OFF_P + 2 * 8 * 2 * 32 * 4;  // tile row maxima [2][4 warps][8] f32
-  static constexpr int OFF_LT = OFF_MX + 2 * 4 * 8 * 4;      // unit row sums [2][4 warps][8] f32
-  static constexpr int OFF_BAR = OFF_LT + 2 * 4 * 8 * 4;     // full[16] | empty[16] | freq[CAP] | rot[CAP]
-  static constexpr int HDR = (OFF_BAR + (32 + 2 * CAP) * 8 + 1023) / 1024 * 1024;
+  static constexpr int OFF_MX = OFF_ML + MLCAP * 8;  // unit-end row maxima [8 warps][8] f32
+  static constexpr int OFF_LT = OFF_MX + 8 * 8 * 4;  // unit-end row sums [8 warps][8] f32
+  static constexpr int OFF_BAR = OFF_LT + 8 * 8 * 4;         // full[16] | empty[16] | freq[CAP] | rot[CAP] | rseen
+  static constexpr int HDR = (OFF_BAR + (33 + 2 * CAP) * 8 + 1023) / 1024 * 1024;
   static constexpr int NSTG0 = (227 * 1024 - 1024 - HDR) / STAGE;
-  static constexpr int NSTG = NSTG0 < 16 ? NSTG0 : 16;
+#ifndef RING_NSTG_CAP
+#define RING_NSTG_CAP 16
+#endif
+  // EVEN: tiles go to the consumer groups by ring-position parity, so every stage has one
+  // fixed consumer group and no waiter can fall two phases behind a stage's mbarrier (a
+  // parity wait cannot tell phase k from phase k + 2; with an odd ring a stage alternated
+  // between the groups and a group running ahead could pass a wait on a stale phase)
+  static constexpr int NSTG = (NSTG0 < RING_NSTG_CAP ? NSTG0 : RING_NSTG_CAP) & ~1;
   static constexpr int SMEM = HDR + NSTG * STAGE + 1024;  // + alignment slack
   static constexpr int THREADS = 10 * 32;                  // producer + 8 consumers + flusher
   static_assert(STAGE % 1024 == 0 && KB % 1024 == 0, "stage alignment (swizzle atoms)");
   static_assert(OFF_RD + kD * 4 <= STAGE && 4 * XH <= STAGE, "R-chunk / text tile fit a stage");
   static_assert(NSTG >= CAP * NCH + 2, "ring must hold the R-chunks and tiles behind them");
+  static_assert(NSTG % 2 == 0, "one consumer group per stage");
   static_assert(RK == 32 || RK == 64, "rank");
   static_assert(G >= 2 && G <= 8, "group");
 };
@@ -157,8 +164,8 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
   uint64_t* empty = full + 16;
   uint64_t* freq = full + 32;
   uint64_t* rotb = freq + C::CAP;  // unit k >= 1 rotated (by the flusher)
+  uint64_t* rseen = rotb + C::CAP;  // the consumers have seen every R-chunk land (first phase)
   float* xch = reinterpret_cast<float*>(sm + C::OFF_X);
-  uint32_t* pbuf = reinterpret_cast<uint32_t*>(sm + C::OFF_P);
   float* mxb = reinterpret_cast<float*>(sm + C::OFF_MX);
   float* ltb = reinterpret_cast<float*>(sm + C::OFF_LT);
 
@@ -185,6 +192,7 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
       mbar_init(&freq[k], 1);
       mbar_init(&rotb[k], 1);
     }
+    mbar_init(rseen, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -354,6 +362,9 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
       __syncwarp();
       if (lane == 0) {
         mbar_arrive_cta(&rotb[k]);  // release: the table entry is written
+        // the consumers wait on this chunk's first phase too; release the stage only after
+        // they have (its next fill is consumed by a group that must not be two phases behind)
+        mbar_wait(rseen, 0);
 #pragma unroll
         for (int ch = 0; ch < C::NCH; ++ch)
           for (int a = 0; a < 4; ++a) mbar_arrive_cta(&empty[(k * C::NCH + ch) % S]);
@@ -409,7 +420,9 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
       }
       mbar_wait(&freq[r], 0);  // this CTA's own state is in `own`
       ++r;
+      stamp(14, gtime());
       while (!arrived()) __nanosleep(64);  // the other contributors (all resident)
+      stamp(15, gtime());
       if (small && !have) prefetch();
       if (small) {
         // merge in slot order (own = slot 0)
@@ -518,6 +531,9 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
     float* scr = xch;  // [8][G][RK + 1] row partials (the group exchange is not in use yet)
     const unsigned char* chs[C::NCH];
     rot_chunks(0, chs);
+    // every R-chunk's first phase is observed by every consumer before the flusher releases
+    // the stage (rseen), so no consumer's later parity wait on it can be two phases behind
+    for (int ps = C::NCH; ps < nu * C::NCH; ++ps) mbar_wait(&full[ps], 0);
     if (warp == 1) stamp(13, gtime());
     {
       float racc[G][RK / 32], bpart[G];
@@ -551,80 +567,67 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
     if (grp == 0 && lane == 0)
 #pragma unroll
       for (int ch = 0; ch < C::NCH; ++ch) mbar_arrive_cta(&empty[ch % S]);
+    if (ci == 0 && lane == 0) mbar_arrive_cta(rseen);
     pos += nu * C::NCH;  // the other units' R-chunks are the flusher's
   }
   if (warp == 1) stamp(1, gtime());
 
+  // per-warp running state over its token slices (all 128 value channels): rows g (q~_hi /
+  // P_hi) and g + 8 (lo) of the 16 eight-channel blocks of O
   uint32_t aq[NKS][4];
   float bg = 0.f, m = -CUDART_INF_F, l = 0.f;
-  float acc[4][4];
+  float acc[16][4];
   bool first_tile = true;
   int nreq = 0;
 
-  // one tile, split over the group's four warps: this warp holds the scores s[NBW][2] (row g)
-  // of its NBW n-blocks (n-block nb0 + i); the tile's row maxima meet through shared memory,
-  // the exponentiated slice is published as P fragments, then O += P . V[:, quarter] over the
-  // NBT n-blocks of the tile
-  uint32_t* pgrp = pbuf + grp * (8 * 2 * 32);
-  float* mxg = mxb + grp * 32;
-  const int gbar = 7 + grp;  // named barrier of this group (128 threads)
-  auto softmax_pv = [&](auto nbw_tag, float (&s)[decltype(nbw_tag)::value][2], int nb0, int NBT, uint32_t v0,
-                        uint32_t vhalf) {
-    constexpr int NBW = decltype(nbw_tag)::value;
-    float tmax = -CUDART_INF_F;
-#pragma unroll
-    for (int j = 0; j < NBW; ++j) tmax = fmaxf(tmax, fmaxf(s[j][0], s[j][1]));
+  // this warp's 16 tokens [tb, tb + 16) of the tile: scores s[nb][.] of its two n-blocks ->
+  // online softmax (row max over the quad; O rescaled only when a row max grows) -> the
+  // probabilities' C fragments ARE the A fragment of O += P . V (hi / lo rows) -> 16 MMAs over
+  // the 128 value channels, B from V rows [tb, tb + 16) by ldmatrix.trans
+  auto softmax_pv = [&](float (&s)[2][2], uint32_t v0, uint32_t vhalf, int tb) {
+    float tmax = fmaxf(fmaxf(s[0][0], s[0][1]), fmaxf(s[1][0], s[1][1]));
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 1));
     tmax = fmaxf(tmax, __shfl_xor_sync(0xffffffffu, tmax, 2));
-    if (c == 0) mxg[qd * 8 + g] = tmax;
-    named_bar(gbar, 128);
-    tmax = fmaxf(fmaxf(mxg[g], mxg[8 + g]), fmaxf(mxg[16 + g], mxg[24 + g]));
     const float mn = live ? fmaxf(m, tmax) : 0.f;
     // nothing valid yet keeps m = -inf: exp2(-inf - -inf) would be NaN
     const bool ok = live && mn != -CUDART_INF_F;
-    const float alpha = ok ? fast_exp2(m - mn) : 0.f;
+    const float alpha = (ok && mn != m) ? fast_exp2(m - mn) : 1.f;
     m = mn;
     l *= alpha;
+    if (__any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 16; ++j)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[j][e] *= alpha;
-#pragma unroll
-    for (int j = 0; j < NBW; ++j) {
-      const float p0 = ok ? fast_exp2(s[j][0] - mn) : 0.f;
-      const float p1 = ok ? fast_exp2(s[j][1] - mn) : 0.f;
-      l += p0 + p1;
-      uint32_t hi, lo;
-      gqa::split2(p0, p1, hi, lo);
-      pgrp[((nb0 + j) * 2 + 0) * 32 + lane] = hi;
-      pgrp[((nb0 + j) * 2 + 1) * 32 + lane] = lo;
+        for (int e = 0; e < 4; ++e) acc[j][e] *= alpha;
     }
-    named_bar(gbar, 128);
-    for (int kt = 0; kt < NBT / 2; ++kt) {
-      uint32_t pa[4];
-      pa[0] = pgrp[(4 * kt + 0) * 32 + lane];
-      pa[1] = pgrp[(4 * kt + 1) * 32 + lane];
-      pa[2] = pgrp[(4 * kt + 2) * 32 + lane];
-      pa[3] = pgrp[(4 * kt + 3) * 32 + lane];
-      const uint32_t tok = 16 * kt + r8 + 8 * (mid & 1);
+    float pr[2][2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t cb = 4 * qd + 2 * h + (mid >> 1);  // 8-column block 0..15
-        const uint32_t addr = v0 + (cb >> 3) * vhalf + gqa::swz<128>(tok, cb & 7);
-        uint32_t b0, b1, b2, b3;
-        gqa::ldsm_x4_t(addr, b0, b1, b2, b3);
-        gqa::mma16816(acc[2 * h], pa, b0, b1);
-        gqa::mma16816(acc[2 * h + 1], pa, b2, b3);
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        pr[nb][e] = ok ? fast_exp2(s[nb][e] - mn) : 0.f;
+        l += pr[nb][e];
       }
+    uint32_t pa[4];
+    gqa::split2(pr[0][0], pr[0][1], pa[0], pa[1]);
+    gqa::split2(pr[1][0], pr[1][1], pa[2], pa[3]);
+    const uint32_t tok = tb + r8 + 8 * (mid & 1);
+#pragma unroll
+    for (int cp = 0; cp < 8; ++cp) {
+      const uint32_t cb = 2 * cp + (mid >> 1);  // 8-channel block 0..15
+      const uint32_t addr = v0 + (cb >> 3) * vhalf + gqa::swz<128>(tok, cb & 7);
+      uint32_t b0, b1, b2, b3;
+      gqa::ldsm_x4_t(addr, b0, b1, b2, b3);
+      gqa::mma16816(acc[2 * cp], pa, b0, b1);
+      gqa::mma16816(acc[2 * cp + 1], pa, b2, b3);
     }
   };
-  // zero rows [t0, t1) of this warp's 32-column quarter of both V halves (128-byte rows):
-  // padding of variable-length units gets p = 0, but 0 * NaN would poison P.V
+  // zero V rows [t0, t1) (all 128 channels, 128-byte rows in two halves) of this warp's own
+  // slice: padding of variable-length units gets p = 0, but 0 * NaN would poison P.V
   auto zero_rows = [&](unsigned char* v0, int half, int t0, int t1) {
-    const int hh = qd >> 1, cbase = 4 * (qd & 1);
-    for (int i = lane; i < (t1 - t0) * 4; i += 32) {
-      const int row = t0 + i / 4, ch = cbase + (i & 3);
-      *reinterpret_cast<uint4*>(v0 + hh * half + gqa::swz<128>(row, ch)) = make_uint4(0u, 0u, 0u, 0u);
+    for (int i = lane; i < (t1 - t0) * 16; i += 32) {
+      const int row = t0 + i / 16, ch = i & 15;
+      *reinterpret_cast<uint4*>(v0 + (ch >> 3) * half + gqa::swz<128>(row, ch & 7)) = make_uint4(0u, 0u, 0u, 0u);
     }
     fence_proxy_async();  // generic writes ordered before the stage's next TMA fill
     __syncwarp();
@@ -646,14 +649,14 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
       m = -CUDART_INF_F;
       l = 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+      for (int j = 0; j < 16; ++j)
 #pragma unroll
         for (int e = 0; e < 4; ++e) acc[j][e] = 0.f;
     }
     const long long k0 = (long long)u * pl.tpu;
     const long long ka = kA > k0 ? kA : k0, kb = kB < k0 + pl.tpu ? kB : k0 + pl.tpu;
     for (long long k = ka; k < kb; ++k, ++pos) {
-      if (((int)(k - ka) & 1) != grp) continue;
+      if ((pos & 1) != grp) continue;  // the stage's fixed consumer group (NSTG even)
       const int st = pos % S;
       mbar_wait(&full[st], (pos / S) & 1);
       if (warp == 1 && first_tile) stamp(2, gtime());
@@ -666,14 +669,13 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
         const int t = j * C::TT;
         const int tn = N - t < C::TT ? N - t : C::TT;
         const int tv = valid_tn(p, u, true, t, tn);
-        if (tv > 0) {
-          constexpr int NBW = C::TT / 32;  // this warp's n-blocks: tokens [16 qd, 16 qd + 16)
-          float s[NBW][2];
+        const int tb = 16 * qd;  // this warp's tokens [tb, tb + 16) of the tile
+        if (tv > tb) {
+          float s[2][2];
 #pragma unroll
-          for (int i = 0; i < NBW; ++i) {
-            const int nb = NBW * qd + i;
+          for (int nb = 0; nb < 2; ++nb) {
             float d[4] = {0.f, 0.f, 0.f, 0.f};
-            const uint32_t row = 8 * nb + r8;
+            const uint32_t row = tb + 8 * nb + r8;
 #pragma unroll
             for (int kp = 0; kp < RK / 32; ++kp) {
               uint32_t b0, b1, b2, b3;
@@ -681,18 +683,19 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
               gqa::mma16816(d, aq[2 * kp], b0, b1);
               gqa::mma16816(d, aq[2 * kp + 1], b2, b3);
             }
-            const int t0 = 8 * nb + 2 * c;
-            s[i][0] = (t0 < tv) ? d[0] + d[2] + bg : -CUDART_INF_F;
-            s[i][1] = (t0 + 1 < tv) ? d[1] + d[3] + bg : -CUDART_INF_F;
+            const int t0 = tb + 8 * nb + 2 * c;
+            s[nb][0] = (t0 < tv) ? d[0] + d[2] + bg : -CUDART_INF_F;
+            s[nb][1] = (t0 + 1 < tv) ? d[1] + d[3] + bg : -CUDART_INF_F;
           }
-          if (tv < tn) zero_rows(stg + C::KB, C::VH, tv, tn);
-          softmax_pv(std::integral_constant<int, NBW>{}, s, NBW * qd, C::TT / 8, sb + C::KB, C::VH);
+          if (tv < tb + 16) zero_rows(stg + C::KB, C::VH, tv, tb + 16);
+          softmax_pv(s, sb + C::KB, C::VH, tb);
         }
       } else {
         const int t = (j - pl.nvt) * C::TX;
         const int tn = M - t < C::TX ? M - t : C::TX;
         const int tv = valid_tn(p, u, false, t, tn);
-        if (tv > 0) {
+        const int tb = 16 * qd;  // warps 0, 1 of the group: tokens [tb, tb + 16) of 32
+        if (qd < C::TX / 16 && tv > tb) {
           // A fragments of q (x scale log2 e, hi/lo rows) from the table
           uint32_t ax[8][4];
           const __nv_bfloat162* q2 = reinterpret_cast<const __nv_bfloat162*>(ent + E::OFF_Q) + gl * (kD / 2);
@@ -703,13 +706,11 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
             gqa::split2(zs * lo.x, zs * lo.y, ax[kk][0], ax[kk][1]);
             gqa::split2(zs * hi.x, zs * hi.y, ax[kk][2], ax[kk][3]);
           }
-          constexpr int NBW = C::TX / 32;  // this warp's n-blocks: tokens [8 qd, 8 qd + 8)
-          float s[NBW][2];
+          float s[2][2];
 #pragma unroll
-          for (int i = 0; i < NBW; ++i) {
-            const int nb = NBW * qd + i;
+          for (int nb = 0; nb < 2; ++nb) {
             float d[4] = {0.f, 0.f, 0.f, 0.f};
-            const uint32_t row = 8 * nb + r8;
+            const uint32_t row = tb + 8 * nb + r8;
 #pragma unroll
             for (int kp = 0; kp < 4; ++kp) {
               const uint32_t chk = 4 * kp + mid;  // 16-byte chunk 0..15 of the 256-byte row
@@ -718,84 +719,87 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
               gqa::mma16816(d, ax[2 * kp], b0, b1);
               gqa::mma16816(d, ax[2 * kp + 1], b2, b3);
             }
-            const int t0 = 8 * nb + 2 * c;
-            s[i][0] = (t0 < tv) ? d[0] + d[2] : -CUDART_INF_F;
-            s[i][1] = (t0 + 1 < tv) ? d[1] + d[3] : -CUDART_INF_F;
+            const int t0 = tb + 8 * nb + 2 * c;
+            s[nb][0] = (t0 < tv) ? d[0] + d[2] : -CUDART_INF_F;
+            s[nb][1] = (t0 + 1 < tv) ? d[1] + d[3] : -CUDART_INF_F;
           }
-          if (tv < tn) zero_rows(stg + 2 * C::XH, C::XH, tv, tn);
-          softmax_pv(std::integral_constant<int, NBW>{}, s, NBW * qd, C::TX / 8, sb + 2 * C::XH, C::XH);
+          if (tv < tb + 16) zero_rows(stg + 2 * C::XH, C::XH, tv, tb + 16);
+          softmax_pv(s, sb + 2 * C::XH, C::XH, tb);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[st]);
     }
-    // ---------------- unit end: merge the two groups, then write out or a CTA partial
-    // this warp's row sum covers its own token slices: the group's sum adds the four
+    // ---------------- unit end: merge the eight warps' states in a fixed order (deterministic)
+    // row sums over the quad; hi + lo rows of O
     float lt = l + __shfl_xor_sync(0xffffffffu, l, 1);
     lt += __shfl_xor_sync(0xffffffffu, lt, 2);
-    if (c == 0) ltb[(grp * 4 + qd) * 8 + g] = lt;
-    float* xq = xch + qd * C::XREC * 32;
     if (u == uA && (warp == 1 || warp == 5)) stamp(warp == 1 ? 8 : 12, gtime());
-    if (grp == 1) {
+    if (c == 0) mxb[ci * 8 + g] = live ? m : -CUDART_INF_F;
+    named_bar(1, 256);  // (A) every warp's row maxima
+    float Mx = -CUDART_INF_F;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
+    for (int w = 0; w < 8; ++w) Mx = fmaxf(Mx, mxb[w * 8 + g]);
+    const float f = (!live || m == -CUDART_INF_F) ? 0.f : fast_exp2(m - Mx);
+    if (c == 0) ltb[ci * 8 + g] = lt * f;
+    float* xrow = xch + ((ci & 3) * 8 + g) * C::XLD + 2 * c;  // slot ci % 4, head g
+    if (ci >= 4) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) xq[(4 * j + e) * 32 + lane] = acc[j][e];
-      xq[16 * 32 + lane] = m;
+      for (int jj = 0; jj < 16; ++jj)
+        *reinterpret_cast<float2*>(xrow + 8 * jj) =
+            make_float2((acc[jj][0] + acc[jj][2]) * f, (acc[jj][1] + acc[jj][3]) * f);
     }
-    named_bar(1, 256);  // group 1's state and every warp's row sum are in shared memory
-    if (grp == 1) {
-      named_bar(1, 256);  // ... and group 0 has read them: the buffers are free again
-      continue;
-    }
-    lt = (ltb[g] + ltb[8 + g]) + (ltb[16 + g] + ltb[24 + g]);
-    {
-      const float l1 = (ltb[32 + g] + ltb[40 + g]) + (ltb[48 + g] + ltb[56 + g]);
-      const float m1 = xq[16 * 32 + lane];
-      const float mn = fmaxf(m, m1);
-      const float f0 = (m == -CUDART_INF_F) ? 0.f : fast_exp2(m - mn);
-      const float f1 = (m1 == -CUDART_INF_F) ? 0.f : fast_exp2(m1 - mn);
-      m = mn;
-      lt = lt * f0 + l1 * f1;
+    named_bar(1, 256);  // (B) warps 4..7 staged; maxima read
+    if (ci < 4) {
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[j][e] = acc[j][e] * f0 + xq[(4 * j + e) * 32 + lane] * f1;
+      for (int jj = 0; jj < 16; ++jj) {
+        float2* x2 = reinterpret_cast<float2*>(xrow + 8 * jj);
+        const float2 o = *x2;
+        *x2 = make_float2((acc[jj][0] + acc[jj][2]) * f + o.x, (acc[jj][1] + acc[jj][3]) * f + o.y);
+      }
     }
-    named_bar(1, 256);
+    named_bar(1, 256);  // (C) slot s = warps s + s + 4
     const int first = pl.cta_of(k0);
     const int count = pl.count(u);
-    const int col = 32 * qd + 2 * c;  // + 8 j
-    if (count == 1) {
-      if (live) {
-        if (p.pout) {
-          float* po = p.pout + ((size_t)u * G + g) * (kD + 2);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<float2*>(po + col + 8 * j) = make_float2(acc[j][0] + acc[j][2], acc[j][1] + acc[j][3]);
-          if (qd == 0 && c == 0) { po[kD] = m; po[kD + 1] = lt; }
-        } else {
-          const float inv = 1.f / lt;
-          float* o = p.out + ((size_t)u * G + g) * kD + col;
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            *reinterpret_cast<float2*>(o + 8 * j) =
-                make_float2((acc[j][0] + acc[j][2]) * inv, (acc[j][1] + acc[j][3]) * inv);
-        }
-      }
-      continue;
-    }
-    // the CTA's partial in slot (this CTA - first) -- or, for the unit this CTA merges itself,
-    // into the idle ring for the flusher -- then a request to the flusher warp
     float* part = p.partials + (size_t)u * pl.cmax * G * kRec;
-    if (live) {
-      float* dst = (u == uB && merger) ? own + g * kRec : part + ((size_t)(c_id - first) * G + g) * kRec;
+    // final: thread ctid -> head hg, channels [4 cq, 4 cq + 4)
+    const int hg = ctid >> 5, cq = lane;
+    if (hg < G) {
+      float4 o4;
+      {
+        const float4 x0 = reinterpret_cast<const float4*>(xch + (0 * 8 + hg) * C::XLD)[cq];
+        const float4 x1 = reinterpret_cast<const float4*>(xch + (1 * 8 + hg) * C::XLD)[cq];
+        const float4 x2 = reinterpret_cast<const float4*>(xch + (2 * 8 + hg) * C::XLD)[cq];
+        const float4 x3 = reinterpret_cast<const float4*>(xch + (3 * 8 + hg) * C::XLD)[cq];
+        o4 = make_float4((x0.x + x1.x) + (x2.x + x3.x), (x0.y + x1.y) + (x2.y + x3.y),
+                         (x0.z + x1.z) + (x2.z + x3.z), (x0.w + x1.w) + (x2.w + x3.w));
+      }
+      float Ls = 0.f, Mh = -CUDART_INF_F;
 #pragma unroll
-      for (int j = 0; j < 4; ++j)
-        *reinterpret_cast<float2*>(dst + col + 8 * j) = make_float2(acc[j][0] + acc[j][2], acc[j][1] + acc[j][3]);
-      if (qd == 0 && c == 0) { dst[kD] = m; dst[kD + 1] = lt; }
+      for (int w = 0; w < 8; ++w) {
+        Ls += ltb[w * 8 + hg];
+        Mh = fmaxf(Mh, mxb[w * 8 + hg]);
+      }
+      if (count == 1 && !p.pout) {
+        const float inv = 1.f / Ls;
+        reinterpret_cast<float4*>(p.out + ((size_t)u * G + hg) * kD)[cq] =
+            make_float4(o4.x * inv, o4.y * inv, o4.z * inv, o4.w * inv);
+      } else {
+        // the unnormalised state: token-shard output, this CTA's partial in slot (this CTA -
+        // first), or -- for the unit this CTA merges itself -- the idle ring for the flusher
+        float* dst = count == 1 ? p.pout + ((size_t)u * G + hg) * (kD + 2)
+                     : (u == uB && merger) ? own + hg * kRec
+                                           : part + ((size_t)(c_id - first) * G + hg) * kRec;
+        if (count == 1) {
+          dst[4 * cq] = o4.x; dst[4 * cq + 1] = o4.y; dst[4 * cq + 2] = o4.z; dst[4 * cq + 3] = o4.w;
+        } else {
+          reinterpret_cast<float4*>(dst)[cq] = o4;
+        }
+        if (cq == 0) { dst[kD] = Mh; dst[kD + 1] = Ls; }
+      }
     }
-    named_bar(6, 128);  // group 0's partial stores precede the request
+    named_bar(1, 256);  // (D) exchange buffers free; partial stores precede the request
+    if (count == 1) continue;
     if (ci == 0 && lane == 0) mbar_arrive_cta(&freq[nreq]);
     ++nreq;
   }

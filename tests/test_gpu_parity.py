@@ -179,6 +179,56 @@ def test_decode_deterministic_and_graph_replay(rk, name, kernel):
         assert torch.equal(out, a)
 
 
+@pytest.mark.parametrize("shape", [(128, 16384, 32), (64, 32768, 32), (64, 32768, 64)])
+def test_ring_long_ranges_repeated(rk, shape):
+    """CTA-ring GQA kernel (kernel 3) with ~225 tiles per CTA, two layers launched back to back
+    several times (the schedule that exposed a two-phase mbarrier parity lag when a ring stage
+    alternated between the consumer groups): no fault, bitwise-identical repeats, and the same
+    result as the per-warp GQA kernel (kernel 5) to fp32 re-association."""
+    import torch
+    U, N, r = shape
+    G, d, M = 7, 128, 128
+    gen = torch.Generator(device="cuda").manual_seed(U * 7 + N + r)
+    layers = []
+    for _ in range(2):
+        layers.append([torch.randn(U, G, d, device="cuda", generator=gen).bfloat16(),
+                       torch.randn(U, N, r, device="cuda", generator=gen).bfloat16(),
+                       torch.randn(U, N, d, device="cuda", generator=gen).bfloat16(),
+                       torch.randn(U, d, r, device="cuda", generator=gen) * 0.1,
+                       torch.randn(U, d, device="cuda", generator=gen) * 0.1,
+                       torch.randn(U, M, d, device="cuda", generator=gen).bfloat16(),
+                       torch.randn(U, M, d, device="cuda", generator=gen).bfloat16()])
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    outs = [torch.empty(U, G, d, device="cuda") for _ in layers]
+    with torch.cuda.stream(s):
+        ws = rk.workspace(rk.make_dims(U, G, d, r, N, M, 0, rk.BF16), rk.OP_DECODE, "cuda", stream=s)
+        first = None
+        for rep in range(6):
+            for lay, o in zip(layers, outs):
+                rk.decode_attn(*lay, out=o, ws=ws, kernel=3, stream=s)
+            s.synchronize()
+            if first is None:
+                first = [o.clone() for o in outs]
+            else:
+                for a, b in zip(first, outs):
+                    assert torch.equal(a, b)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            for lay, o in zip(layers, outs):
+                rk.decode_attn(*lay, out=o, ws=ws, kernel=3, stream=s)
+        for _ in range(4):
+            g.replay()
+        s.synchronize()
+    for a, b in zip(first, outs):
+        assert torch.equal(a, b)
+    for lay, a in zip(layers, first):
+        ref = rk.decode_attn(*lay, kernel=5)
+        torch.cuda.synchronize()
+        err = ((ref - a).abs().amax(-1) / ref.abs().amax(-1)).max().item()
+        assert err <= 1e-5, err
+
+
 # ------------------------------------------------------------------ G-sel
 def _sel_cases():
     rng = np.random.default_rng(5)

@@ -38,6 +38,7 @@ def time_shape(U, G, N, M, r, d=128, reps=30, kernel=0):
         out = torch.empty(U, G, d, device=dev)
         layers.append((q, Kc, V, R, dmu, Kt, Vt, out))
     s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())  # the layers were drawn on the default stream
     with torch.cuda.stream(s):
         ws = rk.workspace(rk.make_dims(U, G, d, r, N, M), rk.OP_DECODE, dev)
         for lay in layers:  # warm (attributes, descriptors)
