@@ -7,8 +7,61 @@ namespace rk {
 
 #include "decode_ring.cuh"
 
-// the CTA-ring GQA kernel (decode_ring.cuh): one CTA per SM over an equal contiguous range of
-// the batch's tiles
+// CTA count of the ring kernel.  Ranges are equal contiguous tile ranges of the batch; the
+// candidates are
+//   * one per SM (at least ceil(tpu / div) tiles each: a unit then spans <= div + 1 CTAs, so
+//     tiny batches use fewer SMs, each with a deeper stream -- Qwen b1 (4 units) 31.4 ->
+//     18.4 us), whose range ends generally fall INSIDE units;
+//   * U * k CTAs, k = min(sms / U, div): every unit cut into k equal pieces (range ends on unit
+//     boundaries or equal fractions, all of a unit's contributors finish together);
+//   * U / k CTAs (U > sms, k | U): k whole units per CTA, no cross-CTA merge at all.
+// Estimate = max(largest range / per-SM stream rate, batch / HBM rate) + a merge penalty:
+// a range end inside a unit leaves some unit with a contributor that reaches it only at the
+// END of its range, so the unit's merge waits a GPU-scope publish (~4 us under the stream's
+// load, traces); equal pieces cost ~2 us; whole units none.  Rates from tools/time_decode.py
+// (qwen_b32_r32: 148 CTAs 36.9 us, 128 = one unit each 32.8 us, 64 = two units each 52.1 us ->
+// ~57 GB/s per SM with the 8-stage ring; long_b16: 128 = halves 108.2 vs 148 111 us).
+static int ring_ctas(int U, int tpu, int sms, int div, int stage_bytes, int cap) {
+  const long long T = (long long)U * tpu;
+  const double r_sm = 57e3, r_hbm = 6.9e6;  // bytes per us
+  auto est = [&](long long Cc, double pen) {
+    if (Cc < 1 || Cc > sms) return 1e30;
+    for (long long c = 0; c < Cc; ++c) {  // every range must touch at most `cap` units
+      const long long kA = T * c / Cc, kB = T * (c + 1) / Cc;
+      if (kB > kA && (kB - 1) / tpu - kA / tpu + 1 > cap) return 1e30;
+    }
+    const double t_sm = (double)((T + Cc - 1) / Cc) * stage_bytes / r_sm;
+    const double t_hbm = (double)T * stage_bytes / r_hbm;
+    return (t_sm > t_hbm ? t_sm : t_hbm) + pen;
+  };
+  const long long minr_req = (tpu + div - 1) / div;
+  long long c0 = T / (minr_req > 0 ? minr_req : 1);
+  if (c0 < 1) c0 = 1;
+  if (c0 > sms) c0 = sms;
+  const bool c0_clean = T % c0 == 0 && (c0 % U == 0 || U % c0 == 0);
+  long long best = c0;
+  double best_t = est(c0, c0_clean ? (c0 > U ? 2.0 : 0.0) : 4.0);
+  auto consider = [&](long long Cc, double pen) {
+    const double t = est(Cc, pen);
+    if (t < best_t) { best_t = t; best = Cc; }
+  };
+  if (U <= sms) {
+    const int k = sms / U < div ? sms / U : div;
+    consider((long long)U * k, k > 1 ? 2.0 : 0.0);
+  } else {
+    for (int k = (U + sms - 1) / sms; k <= cap; ++k)
+      if (U % k == 0) { consider(U / k, 0.0); break; }
+  }
+  static int c_env = [] {
+    const char* e = getenv("ROTATEK_RING_C");  // experiments: force the CTA count
+    return e ? atoi(e) : 0;
+  }();
+  if (c_env > 0 && c_env <= sms) best = c_env;
+  return (int)best;
+}
+
+// the CTA-ring GQA kernel (decode_ring.cuh): one CTA per SM (or per unit / unit piece, see
+// ring_ctas) over an equal contiguous range of the batch's tiles
 template <int RK, int G>
 static int launch_ring_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
   using C = RingCfg<RK, G>;
@@ -19,19 +72,13 @@ static int launch_ring_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   pl.T = (long long)a.U * pl.tpu;
   if ((long long)a.N + a.M >= (1LL << 30) || pl.T >= (1LL << 40)) return -3;
   const int sms = decode_num_sms();
-  // CTAs: one per SM, fewer when a unit would span more CTAs than the merge's shared
-  // (m, l) table holds (tiny batches, e.g. 4 units on 148 SMs)
-  // at least ceil(tpu / div) tiles per CTA (default div 6: a unit spans <= 7 CTAs, so its
-  // merge stays a few slots; tiny batches then use fewer SMs, each with a deeper stream --
-  // Qwen b1 (4 units) 31.4 -> 18.4 us, b8 20.6 us; b32 / long unchanged; tools/time_decode.py)
   static int div_env = [] {
     const char* e = getenv("ROTATEK_RING_DIV");
     return e ? atoi(e) : 6;
   }();
-  const long long minr_req = (pl.tpu + div_env - 1) / (div_env > 0 ? div_env : 6);
-  long long cmax_ctas = pl.T / (minr_req > 0 ? minr_req : 1);
-  if (cmax_ctas < 1) cmax_ctas = 1;
-  for (pl.C = (int)(cmax_ctas < sms ? cmax_ctas : sms);; --pl.C) {
+  const int div = div_env > 0 ? div_env : 6;
+  pl.C = ring_ctas(a.U, pl.tpu, sms, div, C::STAGE, C::CAP);
+  for (;; --pl.C) {
     const long long minr = pl.T / pl.C;  // >= 1 tile per CTA
     pl.cmax = (int)((pl.tpu + minr - 1) / minr) + 1;
     if (pl.cmax > pl.C) pl.cmax = pl.C;
@@ -60,20 +107,18 @@ static int launch_ring_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   DecodeParams p{a.U, a.G, a.d, a.r, a.N, a.M, a.q, a.Kc, a.V, a.R, a.dmu, a.Kt, a.Vt,
                  a.scale * kLog2e, a.out, ws.counters, ws.partials, decode_trace_buffer(), 0, a.pout,
                  a.nR > 0 ? a.nR : a.U, nullptr, nullptr, a.overlap, a.Ms, a.nvu, a.ntu};
-  // cooperative: the merging CTAs wait for their units' other contributors, so every CTA
-  // must be resident (one per SM); plus programmatic serialization with ROTATEK_DECODE_OVERLAP
+  // a plain launch (no CTA ever waits for another: the last contributor of a shared unit
+  // merges it), plus programmatic serialization with ROTATEK_DECODE_OVERLAP
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pl.C);
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[2];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[1].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = a.overlap ? 2 : 1;
+  cfg.numAttrs = a.overlap ? 1 : 0;
   if (cudaLaunchKernelEx(&cfg, kern, maps, p, pl) != cudaSuccess) return -1;
   return 1;
 }

@@ -7,53 +7,53 @@
 //
 //  * Work split.  Every unit is cut into tiles -- ceil(N/64) visual tiles of 64 tokens, then
 //    ceil(M/32) text tiles of 32 full-d tokens -- and the U * tiles_per_unit tiles of the
-//    batch are split into one equal contiguous range per CTA.  Range ends fall on tile
-//    boundaries, so no tensor-map box reads past the range (partial boxes only at unit
-//    ends, where TMA zero-fills and moves no bytes).
+//    batch are split into one equal contiguous range per CTA; the CTA count (decode_ring.cu,
+//    ring_ctas) prefers ranges that end on unit boundaries or equal unit fractions.
 //  * Producer warp (one elected thread) walks the CTA's item sequence
 //        R-chunks of every unit the range touches, then the range's tiles in order
-//    through a ring of NSTG shared-memory stages (20 KB at r = 32: ~180 KB in flight per
+//    through a ring of NSTG (even) shared-memory stages (20 KB at r = 32: 160 KB in flight per
 //    SM).  An R-chunk is 16 KB of R_r[u] rows (1-D bulk copies) plus, in a unit's first
 //    chunk, q[u] (G x 128 bf16) and dmu[u]: the rotation operands are the first bytes the
 //    CTA asks for, so the query rotation never queues behind the tile burst, and the tiles
 //    behind them stream while the rotation runs.  Tiles are tensor-map TMA boxes (K~ [64][r]
 //    with a 64/128-byte swizzle, V as two [64][64] 128-byte-swizzled halves; text K / V as
 //    halves) so ldmatrix reads them without bank conflicts.
-//  * Query rotation (Alg. 2 l.1-2) of all the CTA's units at once, by the eight consumer
-//    warps from the R-chunk stages: warp w sums rows [16w, 16w + 16) of q~ = q R_r and of
-//    b = q . dmu (x scale log2 e) for every head, the eight row partials are added in a fixed
-//    order (deterministic) into the CTA's query table.
-//  * Eight consumer warps = two GROUPS of four.  Group j takes the unit's tiles i with
-//    i % 2 == j; inside a group the four warps take the SAME tile: warp c scores tokens
-//    [16c, 16c + 16) -- S = A . K~^T with mma.sync.m16n8k16, A rows 0..G-1 = q~ rounded to
-//    bf16 (hi), rows 8..8+G-1 = the remainder (lo), so q~ enters with ~16 significant bits --
-//    the four row maxima meet in shared memory (one group barrier), each warp exponentiates
-//    its slice and publishes its P fragments (hi/lo rows, as for q~), and after a second
-//    group barrier warp c accumulates O[16 x 32] += P[16 x 64] . V[:, 32c .. 32c + 32).
-//    The four warps hold identical running maxima, so their row sums simply add at the unit
-//    end, where the two groups' states are merged through shared memory.  (Scoring the whole
-//    tile in every warp measured compute-bound: ~2 tiles/us/SM at any ring depth.)
-//  * Units spanning several CTAs: the unit's FIRST CTA (which reaches it at the END of its
-//    range) merges it.  Every other contributor -- reaching it at the START of its range, or
-//    holding it whole -- has group 0 write its merged partial (acc | m | l per head, slot =
-//    CTA - first CTA) and hands it to a FLUSHER warp that publishes it with a release
-//    reduction on the unit's counter, so no warp ever waits on a global round trip (one
-//    costs ~4-5 us under the decode's own load).  The merging CTA's flusher polls that
-//    counter while its consumers stream and prefetches the published partials, so at the
-//    end the merge (slot order: deterministic) needs no global round trip; it re-arms the
-//    counter (graph-replay safe).  The launch is COOPERATIVE (every CTA resident), so the
-//    merger's wait for a late contributor is a bounded spin.
+//  * Query rotation (Alg. 2 l.1-2) of the range's first unit by the eight consumer warps from
+//    its R-chunk stage(s): warp w sums rows [16w, 16w + 16) of q~ = q R_r and of b = q . dmu
+//    (x scale log2 e) for every head, the eight row partials are added in a fixed order
+//    (deterministic) into the CTA's query table; the flusher warp rotates the other units.
+//  * Eight consumer warps = two GROUPS of four; ring position p belongs to group p % 2 (NSTG
+//    even: every stage has ONE consumer group, so no parity wait can be two phases behind).
+//    In a tile, warp c of the group owns tokens [16c, 16c + 16) for all 128 value channels:
+//    S = A . K~^T with mma.sync.m16n8k16, A rows 0..G-1 = q~ rounded to bf16 (hi), rows
+//    8..8+G-1 = the remainder (lo), so q~ enters with ~16 significant bits; the online
+//    softmax runs on the warp's own slice (row max over a quad, O rescaled only when a row
+//    max grows), and the probabilities' C fragments ARE the A fragment of O += P . V (P hi /
+//    lo rows), B from the V rows by ldmatrix.trans -- no shared-memory exchange and no
+//    barrier per tile.
+//  * Unit end: each warp drops its raw state (O rows hi + lo, row max, row sum) into its
+//    slot and moves on; the FLUSHER warp merges the eight slots in warp order.  A unit held
+//    whole is written out.  A unit shared with other CTAs is published as a partial record
+//    (slot = CTA - the unit's first CTA) with an acq_rel ticket, and the LAST contributor to
+//    arrive merges every record in slot order (deterministic whoever merges; no CTA ever
+//    waits for another, so the launch is a plain one).  For the range's last unit the unit's
+//    first CTA polls the ticket while its consumers stream and prefetches the others'
+//    records; if all are in when its own state is ready it merges at once, no ticket.
 //  * Variable lengths: tiles past a unit's valid length are not loaded at all (the producer
 //    arrives on the stage without bytes), partially valid tiles are masked and their padded
 //    V rows zeroed in shared memory before the P.V product.
 //
-// Why: on Qwen-shaped caches (128 units, 4K tokens) the per-warp design lost ~18 us of a
-// 44 us launch to fixed costs (traces: rotation done at ~3 us, first tile at ~6 us, a 5 us
-// median spread of finish times between the warps of one SM, ~4 us of unit merges over
-// ~6 partials per unit).  Here the rotation rides the ring, the SM's warps share one stream
-// (no within-SM spread), a unit has at most ~3 CTA partials, and an in-range unit boundary
-// costs no global round trip (it cost ~4.5 us per boundary with the ticket and the rotation
-// in line on the compute warps: tools/time_decode.py --trace-ring).
+// Measured (tools/time_decode.py, qwen_b32_r32 = 128 units x 4K tokens): with the consumers
+// doing no math the launch takes 31.2 us (launch gap, first bytes, rotation, tail), with math
+// 32.6 us; one CTA per unit (128 CTAs, no cross-CTA merge) beats 148 equal ranges (36.9 us:
+// the unit whose middle CTA reaches it only at the END of its range waits ~4 us for that
+// CTA's GPU-scope publish under the stream's load).  The per-SM stream saturates near
+// 57-65 GB/s with the 8-stage ring.
+//
+// A stage alternating between the consumer groups lap to lap (odd NSTG, or group = tile
+// parity within a unit) let a group running ahead pass a parity wait on a stage whose fill
+// had not landed -- intermittent hangs / launch failures on ~225-tile ranges
+// (tests/test_gpu_parity.py::test_ring_long_ranges_repeated).
 
 template <int RK, int G>
 struct RingCfg {
@@ -69,19 +69,18 @@ struct RingCfg {
   static constexpr int OFF_RD = OFF_RQ + G * kD * 2; // dmu [128] f32 in chunk 0
   static constexpr int CAP = NCH == 1 ? 4 : 2;       // units per CTA range (query table)
   static constexpr int ENT = QEnt<__nv_bfloat16, RK, G>::BYTES;
-  static constexpr int XLD = kD + 8;                 // exchange row stride (floats): half-warp float2 stores conflict-free
-  static constexpr int XBYTES = 4 * 8 * XLD * 4;     // unit-end exchange [4 slots][8 heads][XLD] f32
+  static constexpr int ULD = kD + 8;                 // unit-end slot row stride (floats): half-warp float2 stores conflict-free
+  static constexpr int USLOT = 8 * G * ULD * 4;      // unit-end warp states [8 warps][G heads][ULD] f32
   static constexpr int RSCR = 8 * G * (RK + 1) * 4;  // rotation partials [8 warps][G][RK + 1]
-  static constexpr int UNI = XBYTES > RSCR ? XBYTES : RSCR;
+  static constexpr int UNI = USLOT > RSCR ? USLOT : RSCR;
   static constexpr int MLCAP = 288;                  // (slot, head) pairs the flusher's merge holds
   static constexpr int PFMAX = 2;                    // partials the flusher prefetches (count - 1)
   static constexpr int OFF_TAB = 0;                  // query table [CAP] entries
-  static constexpr int OFF_X = OFF_TAB + CAP * ENT;  // exchange / rotation scratch (union)
+  static constexpr int OFF_X = OFF_TAB + CAP * ENT;  // unit-end slots / rotation scratch (union)
   static constexpr int OFF_ML = OFF_X + UNI;         // flusher (m, l) table [MLCAP][2] f32
-  static constexpr int OFF_MX = OFF_ML + MLCAP * 8;  // unit-end row maxima [8 warps][8] f32
-  static constexpr int OFF_LT = OFF_MX + 8 * 8 * 4;  // unit-end row sums [8 warps][8] f32
-  static constexpr int OFF_BAR = OFF_LT + 8 * 8 * 4;         // full[16] | empty[16] | freq[CAP] | rot[CAP] | rseen
-  static constexpr int HDR = (OFF_BAR + (33 + 2 * CAP) * 8 + 1023) / 1024 * 1024;
+  static constexpr int OFF_UML = OFF_ML + MLCAP * 8; // unit-end (m, l) per warp and head [8][8][2] f32
+  static constexpr int OFF_BAR = OFF_UML + 8 * 8 * 2 * 4;  // full[16] | empty[16] | rot[CAP] | rseen | ufull | ufree
+  static constexpr int HDR = (OFF_BAR + (35 + CAP) * 8 + 1023) / 1024 * 1024;
   static constexpr int NSTG0 = (227 * 1024 - 1024 - HDR) / STAGE;
 #ifndef RING_NSTG_CAP
 #define RING_NSTG_CAP 16
@@ -162,12 +161,13 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
   unsigned char* ring = sm + C::HDR;
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + C::OFF_BAR);
   uint64_t* empty = full + 16;
-  uint64_t* freq = full + 32;
-  uint64_t* rotb = freq + C::CAP;  // unit k >= 1 rotated (by the flusher)
+  uint64_t* rotb = full + 32;       // unit k >= 1 rotated (by the flusher)
   uint64_t* rseen = rotb + C::CAP;  // the consumers have seen every R-chunk land (first phase)
-  float* xch = reinterpret_cast<float*>(sm + C::OFF_X);
-  float* mxb = reinterpret_cast<float*>(sm + C::OFF_MX);
-  float* ltb = reinterpret_cast<float*>(sm + C::OFF_LT);
+  uint64_t* ufull = rseen + 1;      // unit end n: the eight warps' states are in the slots (phase n)
+  uint64_t* ufree = ufull + 1;      // unit end n: the flusher has read the slots (phase n)
+  float* xch = reinterpret_cast<float*>(sm + C::OFF_X);  // rotation scratch (prologue)
+  float* uslot = xch;                                    // unit-end warp states (after it)
+  float* uml = reinterpret_cast<float*>(sm + C::OFF_UML);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int N = p.N, M = p.M;
@@ -188,11 +188,10 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 4);  // the four warps of the consuming group
     }
-    for (int k = 0; k < C::CAP; ++k) {
-      mbar_init(&freq[k], 1);
-      mbar_init(&rotb[k], 1);
-    }
+    for (int k = 0; k < C::CAP; ++k) mbar_init(&rotb[k], 1);
     mbar_init(rseen, 1);
+    mbar_init(ufull, 8);
+    mbar_init(ufree, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -266,13 +265,6 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
     return;
   }
 
-  // the unit this CTA merges without a ticket when it can: the range's last unit, if the
-  // range holds its head and 1..PFMAX other CTAs hold the rest -- they reach that unit at the
-  // START of their ranges, so their partials are usually published long before this CTA's
-  // consumers get there, and the flusher prefetches them while the CTA streams
-  const int countB = pl.count(uB);
-  const bool merger = countB > 1 && pl.cta_of((long long)uB * pl.tpu) == c_id;
-  float* own = reinterpret_cast<float*>(ring);  // [G][kRec]: this CTA's state of unit uB (idle ring)
 
   // ---------------- query rotation (Alg. 2 l.1-2) of unit k from its R-chunk stage(s), in one
   // fixed summation order whoever computes it: 16-row block w of q~ = q R_r as a pairwise
@@ -370,31 +362,24 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
           for (int a = 0; a < 4; ++a) mbar_arrive_cta(&empty[(k * C::NCH + ch) % S]);
       }
     }
-    // one request per unit of the range that spans several CTAs, in unit order.  Protocol
-    // (the launch is cooperative, so every CTA is resident and a bounded spin is safe): the
-    // unit's FIRST CTA merges it; every other contributor publishes its partial with a
-    // release reduction on the unit's counter and never waits for the result.
+    // then every unit end of the range, in unit order: the eight consumer warps' states
+    // (slots, written without any barrier) are merged here in warp order while the consumers
+    // stream on.  A unit held whole by this CTA is written out.  A unit shared with other CTAs
+    // ("contributors", slot = CTA - the unit's first CTA) is published as a partial record
+    // with a release ticket; the LAST contributor to arrive merges every slot in slot order
+    // (deterministic, whoever merges) -- nobody waits for a late contributor.  Shortcut: for
+    // the range's last unit, the unit's first CTA polls the ticket while its consumers stream
+    // and prefetches the others' partials; if they are all in when its own state is ready it
+    // merges at once with no ticket of its own (same slot-order arithmetic).
     float* ml = reinterpret_cast<float*>(sm + C::OFF_ML);
-    int r = 0;
     for (int u = uA; u <= uB; ++u) {
+      const int ue = u - uA;
       const int count = pl.count(u);
-      if (count == 1) continue;
+      const int first = pl.cta_of((long long)u * pl.tpu);
       float* part = p.partials + (size_t)u * pl.cmax * G * kRec;
-      if (!(u == uB && merger)) {
-        mbar_wait(&freq[r], 0);  // group 0's partial stores are ordered before this (bar + arrive)
-        ++r;
-        if (lane == 0) {
-          fence_acq_rel_gpu();  // cumulative: publishes the CTA's partial before the count
-          red_add_relaxed_gpu(&p.counters[u], 1u);
-        }
-        if (u == uA) stamp(10, gtime());
-        continue;
-      }
-      // ---- this CTA merges unit uB: prefetch the others' partials while the consumers stream
-      // (they reached this unit at the START of their ranges), wait only at the end if needed
       float4 pv[C::PFMAX][G];
       float pm[C::PFMAX][G], pl_[C::PFMAX][G];
-      const bool small = count - 1 <= C::PFMAX;
+      const bool small = u == uB && count > 1 && first == c_id && count - 1 <= C::PFMAX;
       bool have = false;
       auto arrived = [&] {
         unsigned cnt = 0;
@@ -414,99 +399,126 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
           }
         have = true;
       };
-      while (small && !have && !mbar_test(&freq[r], 0)) {
+      while (small && !have && !mbar_test(ufull, ue & 1)) {
         if (arrived()) prefetch();
         else __nanosleep(256);
       }
-      mbar_wait(&freq[r], 0);  // this CTA's own state is in `own`
-      ++r;
-      stamp(14, gtime());
-      while (!arrived()) __nanosleep(64);  // the other contributors (all resident)
-      stamp(15, gtime());
-      if (small && !have) prefetch();
-      if (small) {
-        // merge in slot order (own = slot 0)
+      // ---- this CTA's state of unit u, head gg: the eight warp slots merged in warp order,
+      // channels [4 lane, 4 lane + 4)
+      mbar_wait(ufull, ue & 1);
+      auto own_state = [&](int gg, float4& A, float& Mx, float& Ls) {
+        Mx = -CUDART_INF_F;
+#pragma unroll
+        for (int w = 0; w < 8; ++w) Mx = fmaxf(Mx, uml[(w * 8 + gg) * 2]);
+        Ls = 0.f;
+        A = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const float mw = uml[(w * 8 + gg) * 2];
+          const float f = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - Mx);
+          const float4 v = reinterpret_cast<const float4*>(uslot + (w * G + gg) * C::ULD)[lane];
+          Ls = fmaf(uml[(w * 8 + gg) * 2 + 1], f, Ls);
+          A = make_float4(fmaf(v.x, f, A.x), fmaf(v.y, f, A.y), fmaf(v.z, f, A.z), fmaf(v.w, f, A.w));
+        }
+      };
+      auto put = [&](int gg, const float4& A, float Mx, float Ls) {  // final output or pout state
+        if (p.pout) {
+          float* po = p.pout + ((size_t)u * G + gg) * (kD + 2);
+          po[4 * lane] = A.x; po[4 * lane + 1] = A.y; po[4 * lane + 2] = A.z; po[4 * lane + 3] = A.w;
+          if (lane == 0) { po[kD] = Mx; po[kD + 1] = Ls; }
+        } else {
+          const float inv = 1.f / Ls;
+          reinterpret_cast<float4*>(p.out + ((size_t)u * G + gg) * kD)[lane] =
+              make_float4(A.x * inv, A.y * inv, A.z * inv, A.w * inv);
+        }
+      };
+      if (count == 1) {
+        for (int gg = 0; gg < G; ++gg) {
+          float4 A; float Mx, Ls;
+          own_state(gg, A, Mx, Ls);
+          put(gg, A, Mx, Ls);
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cta(ufree);  // the slots may take the next unit end
+        continue;
+      }
+      if (small && (have || arrived())) {
+        if (!have) prefetch();
+        // every other contributor is in: merge in slot order (this CTA = slot 0), no ticket
 #pragma unroll
         for (int gg = 0; gg < G; ++gg) {
-          const float m0 = own[gg * kRec + kD], l0 = own[gg * kRec + kD + 1];
-          const float4 v0 = reinterpret_cast<const float4*>(own + gg * kRec)[lane];
-          float Mx = fmaxf(-CUDART_INF_F, m0);
+          float4 A; float Mx, Ls;
+          own_state(gg, A, Mx, Ls);
+          float M2 = Mx;
 #pragma unroll
-          for (int s1 = 0; s1 < C::PFMAX; ++s1) Mx = fmaxf(Mx, pm[s1][gg]);
-          float f = (m0 == -CUDART_INF_F) ? 0.f : fast_exp2(m0 - Mx);
-          float Ls = fmaf(l0, f, 0.f);
-          float4 A = make_float4(fmaf(v0.x, f, 0.f), fmaf(v0.y, f, 0.f), fmaf(v0.z, f, 0.f), fmaf(v0.w, f, 0.f));
+          for (int s1 = 0; s1 < C::PFMAX; ++s1) M2 = fmaxf(M2, pm[s1][gg]);
+          float f = (Mx == -CUDART_INF_F) ? 0.f : fast_exp2(Mx - M2);
+          float L2 = fmaf(Ls, f, 0.f);
+          float4 B = make_float4(fmaf(A.x, f, 0.f), fmaf(A.y, f, 0.f), fmaf(A.z, f, 0.f), fmaf(A.w, f, 0.f));
 #pragma unroll
           for (int s1 = 0; s1 < C::PFMAX; ++s1) {
             if (s1 + 1 >= count) continue;
-            f = (pm[s1][gg] == -CUDART_INF_F) ? 0.f : fast_exp2(pm[s1][gg] - Mx);
-            Ls = fmaf(pl_[s1][gg], f, Ls);
-            A.x = fmaf(pv[s1][gg].x, f, A.x);
-            A.y = fmaf(pv[s1][gg].y, f, A.y);
-            A.z = fmaf(pv[s1][gg].z, f, A.z);
-            A.w = fmaf(pv[s1][gg].w, f, A.w);
+            f = (pm[s1][gg] == -CUDART_INF_F) ? 0.f : fast_exp2(pm[s1][gg] - M2);
+            L2 = fmaf(pl_[s1][gg], f, L2);
+            B.x = fmaf(pv[s1][gg].x, f, B.x);
+            B.y = fmaf(pv[s1][gg].y, f, B.y);
+            B.z = fmaf(pv[s1][gg].z, f, B.z);
+            B.w = fmaf(pv[s1][gg].w, f, B.w);
           }
-          if (p.pout) {
-            float* po = p.pout + ((size_t)u * G + gg) * (kD + 2);
-            po[4 * lane] = A.x; po[4 * lane + 1] = A.y; po[4 * lane + 2] = A.z; po[4 * lane + 3] = A.w;
-            if (lane == 0) { po[kD] = Mx; po[kD + 1] = Ls; }
-          } else {
-            const float inv = 1.f / Ls;
-            reinterpret_cast<float4*>(p.out + ((size_t)u * G + gg) * kD)[lane] =
-                make_float4(A.x * inv, A.y * inv, A.z * inv, A.w * inv);
-          }
-        }
-      } else {
-        // many CTAs per unit (tiny batches): own state to slot 0, then the slot-order merge
-        for (int i = lane; i < G * kRec / 4; i += 32)
-          reinterpret_cast<float4*>(part)[i] = reinterpret_cast<const float4*>(own)[i];
-        __syncwarp();
-        for (int i = lane; i < count * G; i += 32) {
-          ml[2 * i] = __ldcg(part + (size_t)i * kRec + kD);
-          ml[2 * i + 1] = __ldcg(part + (size_t)i * kRec + kD + 1);
+          put(gg, B, M2, L2);
         }
         __syncwarp();
-        float Mx[G], Ls[G];
-        float4 A[G];
-#pragma unroll
-        for (int gg = 0; gg < G; ++gg) {
-          Mx[gg] = -CUDART_INF_F;
-          for (int s = 0; s < count; ++s) Mx[gg] = fmaxf(Mx[gg], ml[2 * (s * G + gg)]);
-          Ls[gg] = 0.f;
-          A[gg] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (lane == 0) {
+          mbar_arrive_cta(ufree);
+          p.counters[u] = 0u;  // every other contributor has arrived: re-arm
         }
-        for (int s0 = 0; s0 < count; ++s0) {
-          float4 v[G];
-#pragma unroll
-          for (int gg = 0; gg < G; ++gg)
-            v[gg] = __ldcg(reinterpret_cast<const float4*>(part + ((size_t)s0 * G + gg) * kRec) + lane);
-#pragma unroll
-          for (int gg = 0; gg < G; ++gg) {
-            const int i = s0 * G + gg;
-            const float ms = ml[2 * i];
-            const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx[gg]);
-            Ls[gg] = fmaf(ml[2 * i + 1], f, Ls[gg]);
-            A[gg].x = fmaf(v[gg].x, f, A[gg].x);
-            A[gg].y = fmaf(v[gg].y, f, A[gg].y);
-            A[gg].z = fmaf(v[gg].z, f, A[gg].z);
-            A[gg].w = fmaf(v[gg].w, f, A[gg].w);
-          }
-        }
-#pragma unroll
+        stamp(15, gtime());
+        continue;
+      }
+      // ---- publish this CTA's partial in its slot, then the release ticket
+      {
+        float* dst = part + (size_t)(c_id - first) * G * kRec;
         for (int gg = 0; gg < G; ++gg) {
-          if (p.pout) {
-            float* po = p.pout + ((size_t)u * G + gg) * (kD + 2);
-            po[4 * lane] = A[gg].x; po[4 * lane + 1] = A[gg].y;
-            po[4 * lane + 2] = A[gg].z; po[4 * lane + 3] = A[gg].w;
-            if (lane == 0) { po[kD] = Mx[gg]; po[kD + 1] = Ls[gg]; }
-          } else {
-            const float inv = 1.f / Ls[gg];
-            reinterpret_cast<float4*>(p.out + ((size_t)u * G + gg) * kD)[lane] =
-                make_float4(A[gg].x * inv, A[gg].y * inv, A[gg].z * inv, A[gg].w * inv);
-          }
+          float4 A; float Mx, Ls;
+          own_state(gg, A, Mx, Ls);
+          reinterpret_cast<float4*>(dst + gg * kRec)[lane] = A;
+          if (lane == 0) { dst[gg * kRec + kD] = Mx; dst[gg * kRec + kD + 1] = Ls; }
         }
       }
-      if (lane == 0) p.counters[u] = 0u;  // every other contributor has arrived: re-arm
+      __syncwarp();
+      unsigned old = 0;
+      if (lane == 0) {
+        mbar_arrive_cta(ufree);
+        // release (cumulative: the warp's partial stores, ordered before it by __syncwarp) +
+        // acquire (the last arriver reads the others' partials)
+        old = atom_add_acq_rel_gpu(&p.counters[u], 1u);
+      }
+      old = __shfl_sync(0xffffffffu, old, 0);
+      if (u == uA) stamp(10, gtime());
+      if (old != (unsigned)(count - 1)) continue;
+      // ---- the last contributor: merge every slot in slot order
+      stamp(14, gtime());
+      for (int i = lane; i < count * G; i += 32) {
+        ml[2 * i] = __ldcg(part + (size_t)i * kRec + kD);
+        ml[2 * i + 1] = __ldcg(part + (size_t)i * kRec + kD + 1);
+      }
+      __syncwarp();
+      for (int gg = 0; gg < G; ++gg) {
+        float Mx = -CUDART_INF_F, Ls = 0.f;
+        for (int s0 = 0; s0 < count; ++s0) Mx = fmaxf(Mx, ml[2 * (s0 * G + gg)]);
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int s0 = 0; s0 < count; ++s0) {
+          const int i = s0 * G + gg;
+          const float ms = ml[2 * i];
+          const float f = (ms == -CUDART_INF_F) ? 0.f : fast_exp2(ms - Mx);
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(part + (size_t)i * kRec) + lane);
+          Ls = fmaf(ml[2 * i + 1], f, Ls);
+          A = make_float4(fmaf(v.x, f, A.x), fmaf(v.y, f, A.y), fmaf(v.z, f, A.z), fmaf(v.w, f, A.w));
+        }
+        put(gg, A, Mx, Ls);
+      }
+      __syncwarp();
+      if (lane == 0) p.counters[u] = 0u;  // every contributor has arrived: re-arm
     }
     stamp(4, gtime());
     return;
@@ -578,7 +590,7 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
   float bg = 0.f, m = -CUDART_INF_F, l = 0.f;
   float acc[16][4];
   bool first_tile = true;
-  int nreq = 0;
+  int uend = 0;  // unit ends handed to the flusher
 
   // this warp's 16 tokens [tb, tb + 16) of the tile: scores s[nb][.] of its two n-blocks ->
   // online softmax (row max over the quad; O rescaled only when a row max grows) -> the
@@ -665,13 +677,13 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
       unsigned char* stg = ring + st * C::STAGE;
       const uint32_t sb = smem_u32(stg);
       const int j = (int)(k - k0);
+      float s[2][2];
       if (j < pl.nvt) {
         const int t = j * C::TT;
         const int tn = N - t < C::TT ? N - t : C::TT;
         const int tv = valid_tn(p, u, true, t, tn);
         const int tb = 16 * qd;  // this warp's tokens [tb, tb + 16) of the tile
         if (tv > tb) {
-          float s[2][2];
 #pragma unroll
           for (int nb = 0; nb < 2; ++nb) {
             float d[4] = {0.f, 0.f, 0.f, 0.f};
@@ -706,7 +718,6 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
             gqa::split2(zs * lo.x, zs * lo.y, ax[kk][0], ax[kk][1]);
             gqa::split2(zs * hi.x, zs * hi.y, ax[kk][2], ax[kk][3]);
           }
-          float s[2][2];
 #pragma unroll
           for (int nb = 0; nb < 2; ++nb) {
             float d[4] = {0.f, 0.f, 0.f, 0.f};
@@ -730,78 +741,25 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
       __syncwarp();
       if (lane == 0) mbar_arrive_cta(&empty[st]);
     }
-    // ---------------- unit end: merge the eight warps' states in a fixed order (deterministic)
-    // row sums over the quad; hi + lo rows of O
+    // ---------------- unit end: this warp's raw state (O rows hi + lo, row max, row sum) into
+    // its slot, then on to the next unit -- the flusher merges the eight slots (no barrier)
     float lt = l + __shfl_xor_sync(0xffffffffu, l, 1);
     lt += __shfl_xor_sync(0xffffffffu, lt, 2);
     if (u == uA && (warp == 1 || warp == 5)) stamp(warp == 1 ? 8 : 12, gtime());
-    if (c == 0) mxb[ci * 8 + g] = live ? m : -CUDART_INF_F;
-    named_bar(1, 256);  // (A) every warp's row maxima
-    float Mx = -CUDART_INF_F;
-#pragma unroll
-    for (int w = 0; w < 8; ++w) Mx = fmaxf(Mx, mxb[w * 8 + g]);
-    const float f = (!live || m == -CUDART_INF_F) ? 0.f : fast_exp2(m - Mx);
-    if (c == 0) ltb[ci * 8 + g] = lt * f;
-    float* xrow = xch + ((ci & 3) * 8 + g) * C::XLD + 2 * c;  // slot ci % 4, head g
-    if (ci >= 4) {
+    if (uend > 0) mbar_wait(ufree, (uend - 1) & 1);  // the flusher has read the previous unit end
+    if (live) {
+      float* xrow = uslot + (ci * G + g) * C::ULD + 2 * c;
 #pragma unroll
       for (int jj = 0; jj < 16; ++jj)
-        *reinterpret_cast<float2*>(xrow + 8 * jj) =
-            make_float2((acc[jj][0] + acc[jj][2]) * f, (acc[jj][1] + acc[jj][3]) * f);
-    }
-    named_bar(1, 256);  // (B) warps 4..7 staged; maxima read
-    if (ci < 4) {
-#pragma unroll
-      for (int jj = 0; jj < 16; ++jj) {
-        float2* x2 = reinterpret_cast<float2*>(xrow + 8 * jj);
-        const float2 o = *x2;
-        *x2 = make_float2((acc[jj][0] + acc[jj][2]) * f + o.x, (acc[jj][1] + acc[jj][3]) * f + o.y);
+        *reinterpret_cast<float2*>(xrow + 8 * jj) = make_float2(acc[jj][0] + acc[jj][2], acc[jj][1] + acc[jj][3]);
+      if (c == 0) {
+        uml[(ci * 8 + g) * 2] = m;
+        uml[(ci * 8 + g) * 2 + 1] = lt;
       }
     }
-    named_bar(1, 256);  // (C) slot s = warps s + s + 4
-    const int first = pl.cta_of(k0);
-    const int count = pl.count(u);
-    float* part = p.partials + (size_t)u * pl.cmax * G * kRec;
-    // final: thread ctid -> head hg, channels [4 cq, 4 cq + 4)
-    const int hg = ctid >> 5, cq = lane;
-    if (hg < G) {
-      float4 o4;
-      {
-        const float4 x0 = reinterpret_cast<const float4*>(xch + (0 * 8 + hg) * C::XLD)[cq];
-        const float4 x1 = reinterpret_cast<const float4*>(xch + (1 * 8 + hg) * C::XLD)[cq];
-        const float4 x2 = reinterpret_cast<const float4*>(xch + (2 * 8 + hg) * C::XLD)[cq];
-        const float4 x3 = reinterpret_cast<const float4*>(xch + (3 * 8 + hg) * C::XLD)[cq];
-        o4 = make_float4((x0.x + x1.x) + (x2.x + x3.x), (x0.y + x1.y) + (x2.y + x3.y),
-                         (x0.z + x1.z) + (x2.z + x3.z), (x0.w + x1.w) + (x2.w + x3.w));
-      }
-      float Ls = 0.f, Mh = -CUDART_INF_F;
-#pragma unroll
-      for (int w = 0; w < 8; ++w) {
-        Ls += ltb[w * 8 + hg];
-        Mh = fmaxf(Mh, mxb[w * 8 + hg]);
-      }
-      if (count == 1 && !p.pout) {
-        const float inv = 1.f / Ls;
-        reinterpret_cast<float4*>(p.out + ((size_t)u * G + hg) * kD)[cq] =
-            make_float4(o4.x * inv, o4.y * inv, o4.z * inv, o4.w * inv);
-      } else {
-        // the unnormalised state: token-shard output, this CTA's partial in slot (this CTA -
-        // first), or -- for the unit this CTA merges itself -- the idle ring for the flusher
-        float* dst = count == 1 ? p.pout + ((size_t)u * G + hg) * (kD + 2)
-                     : (u == uB && merger) ? own + hg * kRec
-                                           : part + ((size_t)(c_id - first) * G + hg) * kRec;
-        if (count == 1) {
-          dst[4 * cq] = o4.x; dst[4 * cq + 1] = o4.y; dst[4 * cq + 2] = o4.z; dst[4 * cq + 3] = o4.w;
-        } else {
-          reinterpret_cast<float4*>(dst)[cq] = o4;
-        }
-        if (cq == 0) { dst[kD] = Mh; dst[kD + 1] = Ls; }
-      }
-    }
-    named_bar(1, 256);  // (D) exchange buffers free; partial stores precede the request
-    if (count == 1) continue;
-    if (ci == 0 && lane == 0) mbar_arrive_cta(&freq[nreq]);
-    ++nreq;
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cta(ufull);
+    ++uend;
   }
   if (warp == 1) {
     stamp(3, gtime());
