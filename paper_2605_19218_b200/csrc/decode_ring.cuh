@@ -314,6 +314,38 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
     }
   };
 
+  // unit-end state of this CTA for head gg: the eight warp slots merged in warp order,
+  // channels [4 lane, 4 lane + 4) (flusher, or the consumer warp gg for a range's last unit)
+  auto own_state = [&](int gg, float4& A, float& Mx, float& Ls) {
+    Mx = -CUDART_INF_F;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) Mx = fmaxf(Mx, uml[(w * 8 + gg) * 2]);
+    Ls = 0.f;
+    A = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const float mw = uml[(w * 8 + gg) * 2];
+      const float f = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - Mx);
+      const float4 v = reinterpret_cast<const float4*>(uslot + (w * G + gg) * C::ULD)[lane];
+      Ls = fmaf(uml[(w * 8 + gg) * 2 + 1], f, Ls);
+      A = make_float4(fmaf(v.x, f, A.x), fmaf(v.y, f, A.y), fmaf(v.z, f, A.z), fmaf(v.w, f, A.w));
+    }
+  };
+  auto put = [&](int u, int gg, const float4& A, float Mx, float Ls) {  // final output or pout state
+    if (p.pout) {
+      float* po = p.pout + ((size_t)u * G + gg) * (kD + 2);
+      po[4 * lane] = A.x; po[4 * lane + 1] = A.y; po[4 * lane + 2] = A.z; po[4 * lane + 3] = A.w;
+      if (lane == 0) { po[kD] = Mx; po[kD + 1] = Ls; }
+    } else {
+      const float inv = 1.f / Ls;
+      reinterpret_cast<float4*>(p.out + ((size_t)u * G + gg) * kD)[lane] =
+          make_float4(A.x * inv, A.y * inv, A.z * inv, A.w * inv);
+    }
+  };
+  // the range's last unit, held whole: merged by the consumer warps themselves (one head per
+  // warp, in parallel) instead of the flusher
+  const bool last_whole = pl.count(uB) == 1;
+
   if (warp == 9) {
     // ------------------------------------------------------------------ flusher
     // first: the rotations of units 1.. of the range, in the background of the consumers'
@@ -373,6 +405,7 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
     // merges at once with no ticket of its own (same slot-order arithmetic).
     float* ml = reinterpret_cast<float*>(sm + C::OFF_ML);
     for (int u = uA; u <= uB; ++u) {
+      if (u == uB && last_whole) break;  // the consumers merge it
       const int ue = u - uA;
       const int count = pl.count(u);
       const int first = pl.cta_of((long long)u * pl.tpu);
@@ -406,37 +439,11 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
       // ---- this CTA's state of unit u, head gg: the eight warp slots merged in warp order,
       // channels [4 lane, 4 lane + 4)
       mbar_wait(ufull, ue & 1);
-      auto own_state = [&](int gg, float4& A, float& Mx, float& Ls) {
-        Mx = -CUDART_INF_F;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) Mx = fmaxf(Mx, uml[(w * 8 + gg) * 2]);
-        Ls = 0.f;
-        A = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const float mw = uml[(w * 8 + gg) * 2];
-          const float f = (mw == -CUDART_INF_F) ? 0.f : fast_exp2(mw - Mx);
-          const float4 v = reinterpret_cast<const float4*>(uslot + (w * G + gg) * C::ULD)[lane];
-          Ls = fmaf(uml[(w * 8 + gg) * 2 + 1], f, Ls);
-          A = make_float4(fmaf(v.x, f, A.x), fmaf(v.y, f, A.y), fmaf(v.z, f, A.z), fmaf(v.w, f, A.w));
-        }
-      };
-      auto put = [&](int gg, const float4& A, float Mx, float Ls) {  // final output or pout state
-        if (p.pout) {
-          float* po = p.pout + ((size_t)u * G + gg) * (kD + 2);
-          po[4 * lane] = A.x; po[4 * lane + 1] = A.y; po[4 * lane + 2] = A.z; po[4 * lane + 3] = A.w;
-          if (lane == 0) { po[kD] = Mx; po[kD + 1] = Ls; }
-        } else {
-          const float inv = 1.f / Ls;
-          reinterpret_cast<float4*>(p.out + ((size_t)u * G + gg) * kD)[lane] =
-              make_float4(A.x * inv, A.y * inv, A.z * inv, A.w * inv);
-        }
-      };
       if (count == 1) {
         for (int gg = 0; gg < G; ++gg) {
           float4 A; float Mx, Ls;
           own_state(gg, A, Mx, Ls);
-          put(gg, A, Mx, Ls);
+          put(u, gg, A, Mx, Ls);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive_cta(ufree);  // the slots may take the next unit end
@@ -465,7 +472,7 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
             B.z = fmaf(pv[s1][gg].z, f, B.z);
             B.w = fmaf(pv[s1][gg].w, f, B.w);
           }
-          put(gg, B, M2, L2);
+          put(u, gg, B, M2, L2);
         }
         __syncwarp();
         if (lane == 0) {
@@ -515,7 +522,7 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
           Ls = fmaf(ml[2 * i + 1], f, Ls);
           A = make_float4(fmaf(v.x, f, A.x), fmaf(v.y, f, A.y), fmaf(v.z, f, A.z), fmaf(v.w, f, A.w));
         }
-        put(gg, A, Mx, Ls);
+        put(u, gg, A, Mx, Ls);
       }
       __syncwarp();
       if (lane == 0) p.counters[u] = 0u;  // every contributor has arrived: re-arm
@@ -756,6 +763,15 @@ __global__ void __launch_bounds__(RingCfg<RK, G>::THREADS, 1)
         uml[(ci * 8 + g) * 2] = m;
         uml[(ci * 8 + g) * 2 + 1] = lt;
       }
+    }
+    if (u == uB && last_whole) {
+      named_bar(1, 256);  // every warp's slot is written
+      if (ci < G) {
+        float4 A; float Mx, Ls;
+        own_state(ci, A, Mx, Ls);
+        put(u, ci, A, Mx, Ls);
+      }
+      break;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive_cta(ufull);
