@@ -5,7 +5,7 @@
 //   SAME shared-memory tile read through two MN-major descriptors (128-byte swizzle).
 //   TMA (cp.async.bulk.tensor.3d, SWIZZLE_128B) brings 128-token x 128-channel chunks into a
 //   4-stage ring; one elected thread issues 8 tcgen05.mma (M=128, N=128, K=16) per chunk into
-//   one of two 128-column fp32 accumulators in TMEM; eight epilogue warps drain the other
+//   one of two 128-column fp32 accumulators in TMEM; sixteen epilogue warps drain the other
 //   accumulator with tcgen05.ld and add it into fp64 registers, so each fp32 accumulation
 //   spans at most 256 tokens (exact bf16 products, fp32 per window, fp64 across windows: the
 //   precision scheme of SURVEY Appendix A E-5/E-6).  The column sums are a second MMA per
@@ -13,10 +13,13 @@
 //   pass: ring stages are released by the MMA commit alone).  PERSISTENT: one CTA per SM
 //   walks its (unit, part) items with running stage / window counters, so the next item's
 //   loads and MMAs overlap this item's epilogue.  Out-of-range tokens are zero-filled by TMA.
-//   llava_b32: 290 us -> 214 us (ncu), 3.9 TB/s.
+//   llava_b32: 290 us -> 214 us (ncu), 3.9 TB/s; 16 epilogue warps of 32 columns each (was 8 of
+//   64), TMEM released as soon as a window is in registers, no divisions in the finalize:
+//   229 -> 218 us.  Not the bound any more: dropping the column-sum MMAs or the fp64 drain
+//   arithmetic each gives ~187 us (experiments, r2); F2F.F64.F32 runs at ~16/clk/SM.
 //
-// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
-// warps 2..9 epilogue (TMEM lane quadrant = warp % 4, column half = (warp - 2) / 4).
+// Warp roles (576 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
+// warps 2..17 epilogue (TMEM lane quadrant = warp % 4, column quarter = (warp - 2) / 4).
 #include <cstdio>
 #include <cstring>
 
@@ -29,11 +32,12 @@ namespace rk {
 namespace {
 constexpr int kTK = 128;                 // tokens per chunk (fp32 accumulation window)
 constexpr int kDc = 128;                 // head dim
-constexpr int kStages = 4;
+constexpr int kStages = 4;  // 6 measured slower (254 vs 229 us, llava_b32)
 constexpr int kWin = 2;                  // chunks per fp32 TMEM accumulation window (256 tokens)
 constexpr int kHalfBytes = kTK * 128;    // one 64-channel half: kTK rows x 128 B
 constexpr int kStageBytes = 2 * kHalfBytes;
-constexpr int kThreads = 320;
+constexpr int kEpiWarps = 16;               // 4 per TMEM lane quadrant, 32 accumulator columns each
+constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr int kOnesBytes = 2 * 16 * 128;  // all-ones B tile [16 rows][128 tokens], K-major SW128
 constexpr int kSmem = kStages * kStageBytes + kOnesBytes + 1024 + 256;
 constexpr int kTmemCols = 512;             // 2 x 128 Gram columns + 2 x 16 column-sum columns
@@ -77,7 +81,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 8);
+      mbar_init(&tempty[a], kEpiWarps);
     }
     fence_mbar_init();
     tc::prefetch_tmap(&tmap);
@@ -164,76 +168,75 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
       }
     }
   } else {
-    // ---------------- epilogue: 8 warps
+    // ---------------- epilogue: 16 warps (warp w reads TMEM lane quadrant w % 4; the four
+    // warps of a quadrant take 32 accumulator columns each)
     const int e = warp - 2;
     const int q = warp & 3;        // TMEM lane quadrant this warp may access
-    const int h = e >> 2;          // accumulator column half
+    const int h = e >> 2;          // accumulator column quarter
     const int row = 32 * q + lane;  // output row (channel i)
-    const int et = e * 32 + lane;   // 0..255
+    const int et = e * 32 + lane;   // 0..511
+    constexpr int kEpiThreads = kEpiWarps * 32;
     int gi = 0, gw = 0;  // running chunk / window counters (as the producer and MMA warps)
     for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
     int u, p, c_lo, nch;
     item_range(it, u, p, c_lo, nch);
     (void)c_lo;
-    double acc[64];
+    double acc[32];
 #pragma unroll
-    for (int j = 0; j < 64; ++j) acc[j] = 0.0;
-    double csum = 0.0;  // column sum of channel `row` (warps of column half 0)
+    for (int j = 0; j < 32; ++j) acc[j] = 0.0;
+    double csum = 0.0;  // column sum of channel `row` (warps of column quarter 0)
     for (int i = 0; i < nch; ++i, ++gi) {
       const int a = gw & 1, wph = (gw >> 1) & 1;
       const bool last = (i % kWin) == kWin - 1 || i == nch - 1;
       if (!last) continue;
-      // drain the window's accumulator into fp64 (four loads in flight, one wait)
+      // drain the window's accumulator into fp64 (both loads in flight, one wait)
       mbar_wait(&tfull[a], wph);
       ++gw;
       tc::fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 128 + h * 64;
-      // two halves of 32 columns (fewer live registers next to the 64 fp64 accumulators)
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 128 + h * 32;
       uint32_t r[2][16], rc = 0;
       if (h == 0) tc::ld_32x32b_x1(tmem + ((uint32_t)(32 * q) << 16) + 256 + a * 16, rc);
 #pragma unroll
-      for (int hh = 0; hh < 2; ++hh) {
-#pragma unroll
-        for (int b = 0; b < 2; ++b) tc::ld_32x32b_x16(taddr + (2 * hh + b) * 16, r[b]);
-        tc::ld_wait();
-#pragma unroll
-        for (int b = 0; b < 2; ++b)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) acc[(2 * hh + b) * 16 + j] += (double)__uint_as_float(r[b][j]);
-      }
-      if (h == 0) csum += (double)__uint_as_float(rc);
+      for (int b = 0; b < 2; ++b) tc::ld_32x32b_x16(taddr + b * 16, r[b]);
+      tc::ld_wait();
       tc::fence_before();
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[a]);
+      if (lane == 0) tc::mbar_arrive(&tempty[a]);  // the registers hold the window: free TMEM
+#pragma unroll
+      for (int b = 0; b < 2; ++b)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) acc[b * 16 + j] += (double)__uint_as_float(r[b][j]);
+      if (h == 0) csum += (double)__uint_as_float(rc);
     }
     if (h == 0) colsum_sm[row] = csum;
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(kEpiThreads) : "memory");
     if (fused) {
       // parts == 1: this CTA saw every token of the unit -> finalize here (mu, C, C_q)
       const double* sg = sigma + (size_t)u * kDc;
       const double nu = (double)tsrc.valid(u, N);  // tokens of the unit (per-unit lengths)
-      const double mur = center ? colsum_sm[row] / nu : 0.0;
+      const double inv_nu = 1.0 / nu;
+      const double mur = center ? colsum_sm[row] * inv_nu : 0.0;
       const double sr = sg[row];
-      double* cqr = cq + (size_t)u * kDc * kDc + (size_t)row * kDc + h * 64;
+      double* cqr = cq + (size_t)u * kDc * kDc + (size_t)row * kDc + h * 32;
 #pragma unroll
-      for (int j = 0; j < 64; j += 2) {
-        const int c0 = h * 64 + j;
-        const double m0 = center ? colsum_sm[c0] / nu : 0.0;
-        const double m1 = center ? colsum_sm[c0 + 1] / nu : 0.0;
+      for (int j = 0; j < 32; j += 2) {
+        const int c0 = h * 32 + j;
+        const double m0 = center ? colsum_sm[c0] * inv_nu : 0.0;
+        const double m1 = center ? colsum_sm[c0 + 1] * inv_nu : 0.0;
         const double v0 = sr * sg[c0] * (acc[j] - nu * mur * m0);
         const double v1 = sr * sg[c0 + 1] * (acc[j + 1] - nu * mur * m1);
         *reinterpret_cast<double2*>(cqr + j) = make_double2(v0, v1);
       }
       if (et < kDc) mu[(size_t)u * kDc + et] = center ? colsum_sm[et] / nu : 0.0;
     } else {
-      double* out = covpart + ((size_t)u * parts + p) * kDc * kDc + (size_t)row * kDc + h * 64;
+      double* out = covpart + ((size_t)u * parts + p) * kDc * kDc + (size_t)row * kDc + h * 32;
 #pragma unroll
-      for (int j = 0; j < 64; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
+      for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
       if (et < kDc) colpart[((size_t)u * parts + p) * kDc + et] = colsum_sm[et];
     }
     // every epilogue warp is done reading colsum_sm before the next item's drain may
     // overwrite it (write-after-read across items of this persistent CTA)
-    asm volatile("bar.sync 1, 256;" ::: "memory");
+    asm volatile("bar.sync 1, %0;" ::"r"(kEpiThreads) : "memory");
   }
     }  // items
   tc::fence_before();
