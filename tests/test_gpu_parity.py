@@ -229,6 +229,40 @@ def test_ring_long_ranges_repeated(rk, shape):
         assert err <= 1e-5, err
 
 
+@pytest.mark.parametrize("U,N,M,r", [(4, 4096, 128, 32), (8, 2000, 40, 32), (32, 4096, 128, 32),
+                                     (64, 8192, 0, 32), (100, 1000, 128, 32), (148, 640, 128, 32),
+                                     (256, 700, 16, 32), (300, 333, 33, 32), (128, 1500, 128, 64),
+                                     (24, 3000, 100, 64)])
+def test_ring_plans_match_per_warp_kernel(rk, U, N, M, r):
+    """Every CTA-count plan of the ring kernel (decode_ring.cu: ring_ctas -- one CTA per SM with
+    ranges inside units, U*k equal unit pieces, U/k whole units per CTA; last-arriver and
+    first-CTA shortcut merges, the consumers' last-unit merge) against the per-warp GQA kernel
+    (kernel 5, itself checked against the oracle above), in the normal and partial-state
+    (token-shard) outputs; and bitwise repeatable."""
+    import torch
+    G, d = 7, 128
+    gen = torch.Generator(device="cuda").manual_seed(U * 131 + N + M + r)
+    args = (torch.randn(U, G, d, device="cuda", generator=gen).bfloat16(),
+            torch.randn(U, N, r, device="cuda", generator=gen).bfloat16(),
+            torch.randn(U, N, d, device="cuda", generator=gen).bfloat16(),
+            torch.randn(U, d, r, device="cuda", generator=gen) * 0.1,
+            torch.randn(U, d, device="cuda", generator=gen) * 0.1,
+            torch.randn(U, M, d, device="cuda", generator=gen).bfloat16() if M else None,
+            torch.randn(U, M, d, device="cuda", generator=gen).bfloat16() if M else None)
+    a = rk.decode_attn(*args, kernel=3).clone()
+    b = rk.decode_attn(*args, kernel=3)
+    ref = rk.decode_attn(*args, kernel=5)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    err = ((ref - a).abs().amax(-1) / ref.abs().amax(-1)).max().item()
+    assert err <= 1e-5, err
+    part = rk.decode_attn_partial(*args)  # auto kernel (the ring for this shape)
+    out = rk.merge_partials(part[None])
+    torch.cuda.synchronize()
+    err = ((out - a).abs().amax(-1) / a.abs().amax(-1)).max().item()
+    assert err <= 1e-5, err
+
+
 # ------------------------------------------------------------------ G-sel
 def _sel_cases():
     rng = np.random.default_rng(5)
