@@ -15,8 +15,9 @@
 //   loads and MMAs overlap this item's epilogue.  Out-of-range tokens are zero-filled by TMA.
 //   llava_b32: 290 us -> 214 us (ncu), 3.9 TB/s; 16 epilogue warps of 32 columns each (was 8 of
 //   64), TMEM released as soon as a window is in registers, no divisions in the finalize:
-//   229 -> 218 us.  Not the bound any more: dropping the column-sum MMAs or the fp64 drain
-//   arithmetic each gives ~187 us (experiments, r2); F2F.F64.F32 runs at ~16/clk/SM.
+//   229 -> 218 us; column sums folded into the Gram MMA (N = 144, B = [K | 1] with a constant
+//   ones atom per stage) instead of 8 extra N = 16 MMAs per chunk: 218 -> 191 us.  (fp32 TwoSum
+//   pairs instead of F2F.F64.F32 + DADD in the drain: 203 us, register spills -- not kept.)
 //
 // Warp roles (576 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
 // warps 2..17 epilogue (TMEM lane quadrant = warp % 4, column quarter = (warp - 2) / 4).
@@ -35,12 +36,14 @@ constexpr int kDc = 128;                 // head dim
 constexpr int kStages = 4;  // 6 measured slower (254 vs 229 us, llava_b32)
 constexpr int kWin = 2;                  // chunks per fp32 TMEM accumulation window (256 tokens)
 constexpr int kHalfBytes = kTK * 128;    // one 64-channel half: kTK rows x 128 B
-constexpr int kStageBytes = 2 * kHalfBytes;
+// a stage = the chunk's two 64-channel halves + a third "half" of bf16 ones: the Gram MMA runs
+// with N = 144 (B = [K | 1]), so its columns 128..143 are the column sums sum_n K[n][i]
+constexpr int kStageBytes = 3 * kHalfBytes;
 constexpr int kEpiWarps = 16;               // 4 per TMEM lane quadrant, 32 accumulator columns each
 constexpr int kThreads = (2 + kEpiWarps) * 32;
-constexpr int kOnesBytes = 2 * 16 * 128;  // all-ones B tile [16 rows][128 tokens], K-major SW128
-constexpr int kSmem = kStages * kStageBytes + kOnesBytes + 1024 + 256;
-constexpr int kTmemCols = 512;             // 2 x 128 Gram columns + 2 x 16 column-sum columns
+constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+constexpr int kAccCols = 256;              // TMEM columns per accumulation window (144 used)
+constexpr int kTmemCols = 512;             // 2 windows x kAccCols (128 Gram + 16 column-sum columns used)
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_constant__ CUtensorMap tmap, int N,
@@ -52,8 +55,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
                                                              const __nv_bfloat16* __restrict__ Kg) {
   extern __shared__ unsigned char smraw[];
   unsigned char* sm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(smraw) + 1023) & ~uintptr_t(1023));
-  unsigned char* ones = sm + kStages * kStageBytes;  // 1024-aligned
-  uint64_t* full = reinterpret_cast<uint64_t*>(ones + kOnesBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
@@ -86,10 +88,12 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     fence_mbar_init();
     tc::prefetch_tmap(&tmap);
   }
-  // column sums on the tensor core too: D_col[128 x 16] = K^T . ONES (every column of D_col
-  // is sum_n K[n][i]); the all-ones tile's layout is immaterial (all elements equal)
-  for (int e = threadIdx.x; e < kOnesBytes / 16; e += blockDim.x)
-    reinterpret_cast<uint4*>(ones)[e] = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+  // column sums on the tensor core too: every stage's third half is all ones (never written by
+  // TMA), so D[:, 128 + j] = K^T . ONES = sum_n K[n][i] (all 16 columns equal)
+  for (int st = 0; st < kStages; ++st)
+    for (int e = threadIdx.x; e < kHalfBytes / 16; e += blockDim.x)
+      reinterpret_cast<uint4*>(sm + st * kStageBytes + 2 * kHalfBytes)[e] =
+          make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
   fence_proxy_async();  // generic-proxy writes must be visible to the tensor core (async proxy)
   if (warp == 1) tc::tmem_alloc(tmem_slot, kTmemCols);
   tc::fence_before();
@@ -123,7 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
           const int s = gi % kStages;
           mbar_wait(&empty[s], ((gi / kStages) & 1) ^ 1);
           unsigned char* dst = sm + s * kStageBytes;
-          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          mbar_arrive_expect_tx(&full[s], 2 * kHalfBytes);
           const int tok = (c_lo + i) * kTK;
           tc::tma_load_3d(dst, &tmap, 0, tok, u, &full[s], pol);
           tc::tma_load_3d(dst + kHalfBytes, &tmap, 64, tok, u, &full[s], pol);
@@ -132,9 +136,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 128, true, true);
-      constexpr uint32_t idesc_col = tc::idesc_bf16_f32(128, 16, true, false);
-      const uint32_t obase = smem_u32(ones);
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(128, 144, true, true);  // B = [K | 1]
       int gi = 0, gw = 0;  // running chunk / accumulation-window counters
       for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
         int u, p, c_lo, nch;
@@ -154,10 +156,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
           for (int kk = 0; kk < kTK / 16; ++kk) {
             // MN-major, SWIZZLE_128B: LBO = next 64-channel half, SBO = next 8-token group
             const uint64_t desc = tc::smem_desc(base + kk * 16 * 128, kHalfBytes, 1024, tc::SWZ_128B);
-            tc::mma_bf16(tmem + a * 128, desc, desc, idesc, (first && kk == 0) ? 0u : 1u);
-            const uint64_t od = tc::smem_desc(obase + (kk >> 2) * (kOnesBytes / 2) + (kk & 3) * 32, 16, 1024,
-                                              tc::SWZ_128B);
-            tc::mma_bf16(tmem + 256 + a * 16, desc, od, idesc_col, (first && kk == 0) ? 0u : 1u);
+            tc::mma_bf16(tmem + a * kAccCols, desc, desc, idesc, (first && kk == 0) ? 0u : 1u);
           }
           tc::commit(&empty[s]);
           if (last) {
@@ -193,9 +192,9 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
       mbar_wait(&tfull[a], wph);
       ++gw;
       tc::fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * 128 + h * 32;
+      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * kAccCols + h * 32;
       uint32_t r[2][16], rc = 0;
-      if (h == 0) tc::ld_32x32b_x1(tmem + ((uint32_t)(32 * q) << 16) + 256 + a * 16, rc);
+      if (h == 0) tc::ld_32x32b_x1(tmem + ((uint32_t)(32 * q) << 16) + a * kAccCols + 128, rc);
 #pragma unroll
       for (int b = 0; b < 2; ++b) tc::ld_32x32b_x16(taddr + b * 16, r[b]);
       tc::ld_wait();
