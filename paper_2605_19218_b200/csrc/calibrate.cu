@@ -150,7 +150,11 @@ int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws,
 
 // ============================================================== step 2b/3: finalize
 // mu = colsum / N ; C = S - N mu mu^T (fp64) ; C_q = (sigma sigma^T) (.) C.  Reads only the
-// upper tiles (a <= b), so C_q is exactly symmetric.
+// upper tiles (a <= b), so C_q is exactly symmetric.  One CTA per (unit, 32 x 32 output tile):
+// the source tile (min, max) of the summed partial Grams is staged in shared memory with
+// coalesced row reads, and a lower output tile reads it transposed (a direct read of the
+// lower triangle's mirror element strides by d: 40 us for Qwen b32 before, r2).
+constexpr int kFinT = 32;
 __global__ void __launch_bounds__(256) finalize_kernel(int N, int d, int parts, bool center,
                                                        const double* __restrict__ covpart,
                                                        const double* __restrict__ colpart,
@@ -158,8 +162,9 @@ __global__ void __launch_bounds__(256) finalize_kernel(int N, int d, int parts, 
                                                        double* __restrict__ cq,
                                                        double* __restrict__ mu_out,
                                                        const int32_t* __restrict__ nvu) {
-  extern __shared__ double sh_mu[];  // [d] mu, [d] sigma
+  extern __shared__ double sh_mu[];  // [d] mu, [d] sigma, [kFinT][kFinT + 1] source tile
   double* sh_sig = sh_mu + d;
+  double* tile = sh_sig + d;
   const int u = blockIdx.x;
   if (nvu != nullptr) {  // per-unit token counts (NEXT-2): mu and C over the unit's own tokens
     const int v = nvu[u];
@@ -173,23 +178,35 @@ __global__ void __launch_bounds__(256) finalize_kernel(int N, int d, int parts, 
     if (blockIdx.y == 0) mu_out[(size_t)u * d + j] = m;
     sh_sig[j] = sigma[(size_t)u * d + j];
   }
-  __syncthreads();
-  // blockIdx.y selects a band of rows (grid U x gridDim.y: enough CTAs even for small U)
-  const int rows = (d + gridDim.y - 1) / gridDim.y;
-  const int e0 = blockIdx.y * rows * d, e1 = min(d, (int)(blockIdx.y + 1) * rows) * d;
-  for (int e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-    int i = e / d, j = e % d;
-    int a = min(i, j), b = max(i, j);
+  const int nt = (d + kFinT - 1) / kFinT;
+  const int ti = blockIdx.y / nt, tj = blockIdx.y % nt;
+  const int sa = ti < tj ? ti : tj, sb = ti < tj ? tj : ti;  // source tile (upper)
+  // source tile rows sa*T.., columns sb*T.. of sum_p covpart (coalesced along columns)
+  for (int e = threadIdx.x; e < kFinT * kFinT; e += blockDim.x) {
+    const int r = e / kFinT, c = e % kFinT;
+    const int a = sa * kFinT + r, b = sb * kFinT + c;
     double s = 0.0;
-    for (int p = 0; p < parts; ++p) s += covpart[((size_t)u * parts + p) * d * d + (size_t)a * d + b];
-    double c = s - (double)N * sh_mu[a] * sh_mu[b];
-    cq[(size_t)u * d * d + e] = sh_sig[a] * sh_sig[b] * c;
+    if (a < d && b < d)
+      for (int p = 0; p < parts; ++p) s += covpart[((size_t)u * parts + p) * d * d + (size_t)a * d + b];
+    tile[r * (kFinT + 1) + c] = s;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < kFinT * kFinT; e += blockDim.x) {
+    const int r = e / kFinT, c = e % kFinT;
+    const int i = ti * kFinT + r, j = tj * kFinT + c;
+    if (i >= d || j >= d) continue;
+    const int a = i < j ? i : j, b = i < j ? j : i;  // upper element (a, b)
+    // its place in the source tile: row a - sa*T, column b - sb*T
+    const double s = tile[(a - sa * kFinT) * (kFinT + 1) + (b - sb * kFinT)];
+    const double c2 = s - (double)N * sh_mu[a] * sh_mu[b];
+    cq[(size_t)u * d * d + (size_t)i * d + j] = sh_sig[a] * sh_sig[b] * c2;
   }
 }
 
 int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st, const int32_t* nvu) {
-  finalize_kernel<<<dim3(U, 16), 256, 2 * d * sizeof(double), st>>>(N, d, ws.parts, center, ws.covpart,
-                                                          ws.colpart, ws.sigma, ws.cq, ws.mu, nvu);
+  const int nt = (d + kFinT - 1) / kFinT;
+  finalize_kernel<<<dim3(U, nt * nt), 256, (2 * d + kFinT * (kFinT + 1)) * sizeof(double), st>>>(
+      N, d, ws.parts, center, ws.covpart, ws.colpart, ws.sigma, ws.cq, ws.mu, nvu);
   return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
 }
 
