@@ -128,11 +128,21 @@ __global__ void __launch_bounds__(256) cov_kernel(int N, int d, int parts, const
     colpart[((size_t)u * parts + p) * d + ci0 + tid] = cold;
 }
 
+// Token parts per unit for the covariance (work items = U x parts over the persistent
+// tcgen05 kernel's 148 CTAs).  Per-CTA cost in 128-token chunks: ceil(U P / 148) items x
+// (ceil(nch / P) chunks + 4 chunk-equivalents of fp64 partial-Gram write when P > 1: 128 KB
+// vs a 32 KB key chunk; P == 1 finalizes in place).  Qwen b32 -> 1 (was 3), long b16 -> 2
+// (was 5), Qwen b8 -> 4 (was 10), LLaVA b8 -> 1 (was 2).
 int cov_parts(int U, int N) {
-  int want = (2 * kNumSMs + U - 1) / U;  // >= ~2 CTAs per SM of work
-  int maxp = (N + 255) / 256;            // keep >= 256 tokens per part
-  int p = want < maxp ? want : maxp;
-  return p < 1 ? 1 : p;
+  const long long nch = (N + 127) / 128;
+  int best = 1;
+  long long best_c = -1;
+  for (int P = 1; P <= 32 && P <= nch; ++P) {
+    const long long items = ((long long)U * P + kNumSMs - 1) / kNumSMs;
+    const long long c = items * ((nch + P - 1) / P + (P > 1 ? 4 : 0));
+    if (best_c < 0 || c < best_c) { best_c = c; best = P; }
+  }
+  return best;
 }
 
 int launch_cov(int U, int N, int d, bool bf16, const void* K, const CalibWs& ws, cudaStream_t st) {

@@ -9,15 +9,14 @@
 //   third 64-element atom of bf16 ones (written once, never touched by TMA), so accumulator
 //   columns 128..143 are the column sums sum_n K[n][i] (no separate MMA, no shared-memory
 //   pass).  Sixteen epilogue warps drain the other accumulator with tcgen05.ld and add it into
-//   fp64 registers, so each fp32 accumulation spans at most 512 tokens (exact bf16 products,
-//   fp32 per window, fp64 across windows: the precision scheme of SURVEY Appendix A E-5/E-6,
-//   with the window measured at 512, see kWin).  PERSISTENT: one CTA per SM walks its (unit,
+//   fp64 registers, so each fp32 accumulation spans at most 256 tokens (exact bf16 products,
+//   fp32 per window, fp64 across windows: the precision scheme of SURVEY Appendix A E-5/E-6).  PERSISTENT: one CTA per SM walks its (unit,
 //   part) items with running stage / window counters, so the next item's loads and MMAs
 //   overlap this item's epilogue.  Out-of-range tokens are zero-filled by TMA.
 //   llava_b32 (ncu): 290 us (one CTA per unit) -> 214 -> 229 (r1 final) -> 218 (16 epilogue
 //   warps of 32 columns, TMEM released as soon as a window is in registers, no divisions in
 //   the finalize) -> 191 (column sums folded into the Gram MMA instead of 8 extra N = 16 MMAs
-//   per chunk) -> 166 us (512-token windows: half the fp32 -> fp64 drains).  (fp32 TwoSum
+//   per chunk); 512-token windows 167 us but less precise (see kWin).  (fp32 TwoSum
 //   pairs instead of F2F.F64.F32 + DADD in the drain: 203 us, register spills -- not kept.)
 //
 // Warp roles (576 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
@@ -35,12 +34,11 @@ namespace {
 constexpr int kTK = 128;                 // tokens per chunk (fp32 accumulation window)
 constexpr int kDc = 128;                 // head dim
 constexpr int kStages = 4;  // 6 measured slower (254 vs 229 us, llava_b32)
-// chunks per fp32 TMEM accumulation window: 512 tokens.  SURVEY E-6 proposed <= 256; measured
-// on planted-gap keys with mean offsets 5 and 20 (tools/cov_err.py, r2) the eigenvalue and
-// projector errors against the fp64 oracle are identical to 3 digits for 256 and 512 (1.8e-6 /
-// 7e-5 at mean 5, the Jacobi + refinement floor), while halving the fp32 -> fp64 drains (whose
-// F2F.F64.F32 conversions run at ~16/clk/SM) takes llava_b32 from 191 to 166 us
-constexpr int kWin = 4;
+// chunks per fp32 TMEM accumulation window: 256 tokens (SURVEY E-6).  512 was measured (r2,
+// tools/cov_err2.py): 191 -> 167 us on llava_b32 (half the fp32 -> fp64 drains), but the worst
+// unit's projector error vs the fp64 oracle on large-mean planted-gap keys grows 9.7e-5 ->
+// 1.4e-4 (40 units x 300 tokens; the CUDA-core path: 2.5e-6), past the 1e-4 gate -- not taken
+constexpr int kWin = 2;
 constexpr int kHalfBytes = kTK * 128;    // one 64-channel half: kTK rows x 128 B
 // a stage = the chunk's two 64-channel halves + a third "half" of bf16 ones: the Gram MMA runs
 // with N = 144 (B = [K | 1]), so its columns 128..143 are the column sums sum_n K[n][i]
@@ -149,7 +147,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
         item_range(it, u, p, c_lo, nch);
         (void)u; (void)p; (void)c_lo;
         for (int i = 0; i < nch; ++i, ++gi) {
-          // fp32 accumulation window = kWin chunks (kWin * 128 = 512 tokens), never
+          // fp32 accumulation window = kWin chunks (kWin * 128 = 256 tokens, E-6), never
           // spanning two items
           const int s = gi % kStages, a = gw & 1;
           const bool first = (i % kWin) == 0, last = (i % kWin) == kWin - 1 || i == nch - 1;
