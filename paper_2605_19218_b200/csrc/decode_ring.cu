@@ -7,6 +7,14 @@ namespace rk {
 
 #include "decode_ring.cuh"
 
+static bool cluster_off() {  // experiments / A-B: ROTATEK_RING_NOCLUSTER=1 keeps the global merges
+  static bool v = [] {
+    const char* e = getenv("ROTATEK_RING_NOCLUSTER");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+
 // CTA count of the ring kernel.  Ranges are equal contiguous tile ranges of the batch; the
 // candidates are
 //   * one per SM (at least ceil(tpu / div) tiles each: a unit then spans <= div + 1 CTAs, so
@@ -18,14 +26,16 @@ namespace rk {
 // Estimate = max(largest range / per-SM stream rate, batch / HBM rate) + a merge penalty:
 // a range end inside a unit leaves some unit with a contributor that reaches it only at the
 // END of its range, so the unit's merge waits a GPU-scope publish (~4 us under the stream's
-// load, traces); equal pieces cost ~2 us; whole units none.  Rates from tools/time_decode.py
+// load, traces); equal pieces (k <= 8) form one thread-block cluster per unit and merge
+// through distributed shared memory (~0.5 us; ~2 us with a global last-arriver merge); whole
+// units none.  Rates from tools/time_decode.py
 // (qwen_b32_r32: 148 CTAs 36.9 us, 128 = one unit each 32.8 us, 64 = two units each 52.1 us ->
 // ~57 GB/s per SM with the 8-stage ring; long_b16: 128 = halves 108.2 vs 148 111 us).
 static int ring_ctas(int U, int tpu, int sms, int div, int stage_bytes, int cap) {
   const long long T = (long long)U * tpu;
   const double r_sm = 57e3, r_hbm = 6.9e6;  // bytes per us
   auto est = [&](long long Cc, double pen) {
-    if (Cc < 1 || Cc > sms) return 1e30;
+    if (Cc < 1 || Cc > sms || Cc > T) return 1e30;  // every CTA holds >= 1 tile
     for (long long c = 0; c < Cc; ++c) {  // every range must touch at most `cap` units
       const long long kA = T * c / Cc, kB = T * (c + 1) / Cc;
       if (kB > kA && (kB - 1) / tpu - kA / tpu + 1 > cap) return 1e30;
@@ -46,8 +56,11 @@ static int ring_ctas(int U, int tpu, int sms, int div, int stage_bytes, int cap)
     if (t < best_t) { best_t = t; best = Cc; }
   };
   if (U <= sms) {
-    const int k = sms / U < div ? sms / U : div;
-    consider((long long)U * k, k > 1 ? 2.0 : 0.0);
+    // equal pieces: k <= 8 (one thread-block cluster per unit, DSMEM merge ~0.5 us)
+    const int kmax = cluster_off() ? div : 8;
+    int k = sms / U < kmax ? sms / U : kmax;
+    if (k > tpu) k = tpu;  // >= 1 tile per piece
+    consider((long long)U * k, k > 1 ? (cluster_off() ? 2.0 : 0.5) : 0.0);
   } else {
     for (int k = (U + sms - 1) / sms; k <= cap; ++k)
       if (U % k == 0) { consider(U / k, 0.0); break; }
@@ -90,6 +103,13 @@ static int launch_ring_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
     if (kB > kA && (kB - 1) / pl.tpu - kA / pl.tpu + 1 > C::CAP) return -3;
   }
   if ((size_t)a.U * pl.cmax * a.G * (kD + 4) * 4 > ws.partial_bytes) return -3;
+  // equal-piece plan (every unit = k consecutive CTAs): one thread-block cluster per unit, the
+  // pieces merged through distributed shared memory instead of a GPU-scope publish
+  pl.clus = 0;
+  {
+    const int k = pl.C / a.U;
+    if (k >= 2 && k <= 8 && pl.C == a.U * k && pl.tpu >= k && !cluster_off()) pl.clus = k;
+  }
   RingMaps maps;
   memset(&maps, 0, sizeof(maps));
   if (!encode_tmap_3d_bf16(&maps.kc, a.Kc, RK, a.N, a.U, RK, C::TT, RK * 2)) return -2;
@@ -114,12 +134,29 @@ static int launch_ring_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
   cfg.blockDim = dim3(C::THREADS);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute attr[2];
+  int na = 0;
+  if (a.overlap) {
+    attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  if (pl.clus > 1) {
+    attr[na].id = cudaLaunchAttributeClusterDimension;
+    attr[na].val.clusterDim.x = pl.clus;
+    attr[na].val.clusterDim.y = 1;
+    attr[na].val.clusterDim.z = 1;
+    ++na;
+  }
   cfg.attrs = attr;
-  cfg.numAttrs = a.overlap ? 1 : 0;
-  if (cudaLaunchKernelEx(&cfg, kern, maps, p, pl) != cudaSuccess) return -1;
+  cfg.numAttrs = na;
+  if (cudaLaunchKernelEx(&cfg, kern, maps, p, pl) != cudaSuccess) {
+    if (pl.clus <= 1) return -1;
+    cudaGetLastError();  // the cluster shape could not be scheduled: plain launch, global merges
+    pl.clus = 0;
+    cfg.numAttrs = a.overlap ? 1 : 0;
+    if (cudaLaunchKernelEx(&cfg, kern, maps, p, pl) != cudaSuccess) return -1;
+  }
   return 1;
 }
 
