@@ -527,10 +527,15 @@ int launch_decode(const DecodeArgs& a, const DecodeWs& ws, int splits, int kerne
   }
   const bool fast_ok = fast_supported(a);
   const bool gqa_ok = gqa_supported(a);
-  if ((kernel == 2 && !fast_ok) || ((kernel == 3 || kernel == 5) && !gqa_ok)) return -2;
+  const bool ring1_ok = a.bf16 && a.d == kD && (a.r == 32 || a.r == 64) && a.G == 1 && (a.M == 0 || (a.Kt && a.Vt));
+  if ((kernel == 2 && !fast_ok) || (kernel == 3 && !gqa_ok && !ring1_ok) || (kernel == 5 && !gqa_ok)) return -2;
   // -3: the streaming kernels' CTA query table cannot hold the units of one CTA range
   // (tiny units, e.g. N + M < ~100 tokens); the generic kernel handles those shapes
-  if (kernel == 3 || (kernel == 0 && gqa_ok && splits <= 0)) {
+  // G = 1: the CTA-ring kernel for small batches (<= 2 units per SM: one CTA per unit or unit
+  // piece, DSMEM merges), the per-warp CUDA-core kernel for large ones (LLaVA b32: 1.02 of the
+  // copy peak; the ring's query table holds <= 4 units per CTA)
+  const bool ring1_auto = ring1_ok && a.U <= 2 * decode_num_sms();
+  if (kernel == 3 || (kernel == 0 && (gqa_ok || ring1_auto) && splits <= 0)) {
     const int rc = launch_ring(a, ws, st);
     if (rc != -3) return rc;
     if (kernel == 3) return -2;

@@ -163,6 +163,7 @@ static int launch_ring_cfg(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t
 template <int RK>
 static int launch_ring_rk(const DecodeArgs& a, const DecodeWs& ws, cudaStream_t st) {
   switch (a.G) {
+    case 1: return launch_ring_cfg<RK, 1>(a, ws, st);
     case 2: return launch_ring_cfg<RK, 2>(a, ws, st);
     case 4: return launch_ring_cfg<RK, 4>(a, ws, st);
     case 7: return launch_ring_cfg<RK, 7>(a, ws, st);

@@ -103,7 +103,7 @@ struct RingCfg {
   static_assert(NSTG >= CAP * NCH + 2, "ring must hold the R-chunks and tiles behind them");
   static_assert(NSTG % 2 == 0, "one consumer group per stage");
   static_assert(RK == 32 || RK == 64, "rank");
-  static_assert(G >= 2 && G <= 8, "group");
+  static_assert(G >= 1 && G <= 8, "group");
 };
 
 struct RingMaps {

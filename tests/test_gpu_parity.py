@@ -767,8 +767,8 @@ def test_appendable_text_segment_multistep(rk, name):
 
 
 def test_debug_decode_trace_stamps(rk):
-    """Diagnostics hook: the streaming kernels stamp per-warp %globaltimer values in order
-    (start <= rotated <= first tile <= loop end <= end) and the tile count."""
+    """Diagnostics hook: the per-warp streaming kernel (kernel 2) stamps per-warp %globaltimer
+    values in order (start <= rotated <= first tile <= loop end <= end) and the tile count."""
     import torch
     cfg = SMALL["llava_small"]
     w = make_workload(cfg)
@@ -779,7 +779,7 @@ def test_debug_decode_trace_stamps(rk):
         rk.decode_attn(to_torch(w["q"]), _as_dev(Kt, "bf16"), to_torch(w["V"]),
                        torch.from_numpy(R.astype(np.float32)).cuda(),
                        torch.from_numpy(dmu.astype(np.float32)).cuda(), to_torch(w["Ktext"]),
-                       to_torch(w["Vtext"]))
+                       to_torch(w["Vtext"]), kernel=2)
         torch.cuda.synchronize()
     finally:
         rk.debug_decode_trace(None)
@@ -807,8 +807,10 @@ def test_decode_variable_lengths(rk, name, nv, nt, kernel, fill):
     header allows any padding: masked V rows must not reach the tensor-core P.V either)."""
     import torch
     cfg = SMALL[name].with_(h_kv=len(nv))
-    if kernel in (3, 5) and cfg.group == 1 or kernel == 4 and (cfg.head_dim != 128 or cfg.rank != 32):
-        pytest.skip("kernel not built for this shape (stealing: d = 128, r = 32)")
+    ring_ok = cfg.head_dim == 128 and cfg.rank in (32, 64) and cfg.group in (1, 2, 4, 7, 8)
+    if (kernel == 3 and not ring_ok or kernel == 5 and (cfg.group == 1 or not ring_ok)
+            or kernel == 4 and (cfg.head_dim != 128 or cfg.rank != 32)):
+        pytest.skip("kernel not built for this shape (ring: d = 128, r in {32, 64}; stealing: r = 32)")
     w = make_workload(cfg)
     R, dmu, Kt = _cache_from_oracle(cfg, w, "bf16")
     q, V = w["q"].f64(), w["V"].f64()
