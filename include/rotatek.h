@@ -250,10 +250,12 @@ rotatek_status rotatek_decode_attn(const rotatek_dims* dims, const void* q, cons
  * the same up to fp32 re-association for every split count (App. C "standard
  * online-softmax merge").  `kernel` forces the implementation:
  * 0 auto, 1 the generic kernel (any d, r, G), 2 the TMA-pipelined CUDA-core streaming
- * kernel, 3 the tensor-core GQA kernel (one CTA per unit, per equal unit piece or per SM,
- * each streaming a shared TMA ring; bf16, d = 128, r in {32, 64}, G in {2, 4, 7, 8}; shared
- * units merged by their last contributor in slot order, so bit-reproducible), 4 the
- * streaming kernels with work stealing
+ * kernel, 3 the tensor-core CTA-ring kernel (one CTA per unit, per equal unit piece or per
+ * SM, each streaming a shared TMA ring; bf16, d = 128, r in {32, 64}, G in {1, 2, 4, 7, 8};
+ * unit pieces merged in slot order through distributed shared memory (a thread-block
+ * cluster per unit) or by their last contributor, so bit-reproducible; the automatic choice
+ * for G >= 2 and for G = 1 batches of <= 2 units per SM), 4 the streaming kernels with work
+ * stealing
  * (bf16, d = 128, r = 32, G in {1, 7}; merges in arrival order, so results are
  * reproducible to fp32 re-association, not bit for bit), 5 the per-warp tensor-core GQA
  * kernel of ABI version 1 (same shapes as 3) -- UNSUPPORTED if the shape has none.  Used
