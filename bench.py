@@ -655,8 +655,10 @@ def run_ours(args):
                      # frac > 1 is possible: the measured peak is a read+write copy, this
                      # kernel is a read-dominated stream (99.7 % reads, ncu)
                      "algorithmic_bytes_per_launch": bytes_layer,
+                     # the automatic choice (decode.cu launch_decode): the CTA ring for
+                     # G >= 2 and for G = 1 batches of <= 2 units per SM
                      "kernel": ("rotatek decode (decode_fast_kernel: cp.async.bulk warp streaming, "
-                                "CUDA cores)" if cfg.group == 1 else
+                                "CUDA cores)" if cfg.group == 1 and cfg.units > 2 * 148 else
                                 "rotatek decode (decode_ring_kernel: CTA ring, tensor-map TMA, "
                                 "mma.sync)")},
         "decode_tflops": round(decode_flops(cfg) / (us_layer * 1e-6) / 1e12, 3),

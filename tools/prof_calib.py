@@ -1,5 +1,6 @@
 #!/usr/bin/env python
-"""One calibrate (Jacobi) + one calibrate_subspace call on a config, for ncu launch lists.
+"""One calibrate (Jacobi) + one calibrate_subspace + one compress call on a config, for ncu
+launch lists and captures.
     ncu --metrics gpu__time_duration.sum python tools/prof_calib.py llava_b32"""
 import os
 import sys
@@ -22,7 +23,8 @@ def dev(t):
 
 K, Qw = dev(w["K"]), dev(w["Qw"])
 V0 = torch.from_numpy(draw_v0(cfg)).cuda()
-rk.calibrate(K, Qw, cfg.rank)
+cal = rk.calibrate(K, Qw, cfg.rank)
 rk.calibrate_subspace(K, Qw, V0)
+rk.compress_kv(K, cal["R"])
 torch.cuda.synchronize()
 print("done")

@@ -87,7 +87,7 @@ traffic["_source"] = ("ncu --set full --clock-control none (tools/profile_all.sh
                       "dram__bytes_read.sum + dram__bytes_write.sum; per-config 'capture' names the file")
 lines = ["| config | kernel | ncu time (us) | dram read+write (MB) | alg. bytes (MB) | traffic/alg | "
          "DRAM % peak | SM issue % | regs |", "|---|---|---|---|---|---|---|---|---|"]
-for cfg in ("llava_b32", "qwen_b32_r32", "joint_b64", "long_b16"):
+for cfg in ("llava_b32", "qwen_b32_r32", "joint_b64", "long_b16", "qwen_b32_r64", "llava_b8", "qwen_b8_r32"):
     p = os.path.join(src, f"ncu_decode_{cfg}_{tag}_raw.csv")
     if not os.path.exists(p):
         continue
@@ -125,7 +125,7 @@ if os.path.exists(p):
 # launch lists: share of the decode kernel in one bench step
 print("\n| config | launches | decode share of step (ncu, serialised) | top kernels (us) |")
 print("|---|---|---|---|")
-for cfg in ("llava_b32", "qwen_b32_r32", "joint_b64", "long_b16"):
+for cfg in ("llava_b32", "qwen_b32_r32", "joint_b64", "long_b16", "qwen_b32_r64", "llava_b8", "qwen_b8_r32"):
     p = os.path.join(src, f"launches_{cfg}_{tag}.csv")
     if not os.path.exists(p):
         continue
