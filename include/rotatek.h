@@ -79,6 +79,12 @@ enum {
                                      Jacobi followed by one fp64 refinement step
                                      (B = V0^T C_q V0, lambda = diag B, V = V0 (I + W) with
                                      the first-order correction W_ij = B_ij / (B_jj - B_ii)) */
+  ROTATEK_EIG_TWOSIDED = 1u << 3, /* d = 128, fp32 solve: use the two-sided packed-triangle
+                                     Jacobi (A and V in shared memory) instead of the default
+                                     one-sided (Hestenes) Jacobi on C_q with the columns in
+                                     registers.  Either is followed by the fp64 refinement; the
+                                     default re-solves with the two-sided kernel any unit whose
+                                     C_q has a (near-)null column (info -2 internally)      */
   ROTATEK_SIMT_ONLY = 1u << 8,    /* use the CUDA-core (SIMT) kernels instead of the tcgen05
                                      tensor-core ones (A/B tests and benches)           */
   ROTATEK_DEFAULT_FLAGS = (1u << 0) | (1u << 1)

@@ -567,9 +567,11 @@ __global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* 
                                                                   float* __restrict__ lam_out,
                                                                   float* __restrict__ vecs,
                                                                   int32_t* __restrict__ jinfo, float tol,
-                                                                  int max_sweeps) {
+                                                                  int max_sweeps, int only_flagged) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr int d = DC, h = DC / 2, ld = DC + 1;
+  // fallback pass behind the one-sided solver (hestenes.cu): only units it marked -2
+  if (only_flagged && jinfo[blockIdx.x] != -2) return;
   constexpr int np = d * (d + 1) / 2, nblk = h * (h + 1) / 2;
   constexpr int nth = kJPThreads;
   const int u = blockIdx.x, tid = threadIdx.x;
@@ -736,6 +738,12 @@ __global__ void __launch_bounds__(kJPThreads, 2) jacobi32p_kernel(const double* 
 // B is diagonal up to the fp32 solver's residual eps ~ 1e-6 ||C||, so the step leaves an
 // O(eps^2 / gap^2) error: fp64-quality projectors at the cost of three 128^3 fp64 GEMMs.
 constexpr int kRefThreads = 256;
+// A pair is corrected only if |W_ij| < kRefMaxW: the step is first order, so it leaves an
+// O(W^2) loss of orthonormality; larger W means a near-degenerate pair (relative gap below
+// ~1e3 x the fp32 solver's residual) whose eigenvectors are not determined anyway -- left as
+// the solver returned them, orthonormal to its residual.  (0.1 here let the full basis of a
+// 96-fold cluster drift 1e-2 from orthonormal with the two-sided solver.)
+constexpr double kRefMaxW = 1e-3;
 
 __global__ void __launch_bounds__(kRefThreads) refine_kernel(int d, const double* __restrict__ cq,
                                                               const float* __restrict__ v0g,
@@ -820,7 +828,7 @@ __global__ void __launch_bounds__(kRefThreads) refine_kernel(int d, const double
     const double gap = diag[j] - diag[i];
     double w;
     if (i == j) w = 0.5 * (1.0 - Gg[e]);
-    else if (fabs(gap) > 1e-12 * bmax && fabs(num) < 0.1 * fabs(gap)) w = num / gap;
+    else if (fabs(gap) > 1e-12 * bmax && fabs(num) < kRefMaxW * fabs(gap)) w = num / gap;
     else w = 0.0;
     T[e] = w;
   }
@@ -961,7 +969,7 @@ __global__ void __launch_bounds__(kRefSmThreads, 1) refine_smem_kernel(const dou
         const double gap = diag[j] - diag[i];
         double w;
         if (i == j) w = 0.5 * (1.0 - Gv[a][b]);
-        else if (fabs(gap) > 1e-12 * bmax && fabs(num) < 0.1 * fabs(gap)) w = num / gap;
+        else if (fabs(gap) > 1e-12 * bmax && fabs(num) < kRefMaxW * fabs(gap)) w = num / gap;
         else w = 0.0;
         W[k][a][b] = w;
       }
@@ -1017,7 +1025,10 @@ __global__ void __launch_bounds__(kRefSmThreads, 1) refine_smem_kernel(const dou
   for (int j = tid; j < d; j += kRefSmThreads) lam_out[(size_t)u * d + j] = (float)diag[j];
 }
 
-int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st) {
+int launch_hestenes(int U, const double* cq, float* lam, float* v32, int32_t* jinfo, float tol,
+                    float qstop, int max_sweeps, cudaStream_t st);
+
+int launch_jacobi(int U, int d, bool fp64, bool twosided, const CalibWs& ws, cudaStream_t st) {
   if (fp64) {
     size_t sm = jacobi_smem_bytes(d, true);
     cudaFuncSetAttribute(jacobi_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1032,7 +1043,11 @@ int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st) {
   if (d == 128) {
     const size_t smp = jacobi32p_smem_bytes(d);
     cudaFuncSetAttribute(jacobi32p_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
-    jacobi32p_kernel<128><<<U, kJPThreads, smp, st>>>(ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
+    // default: one-sided Jacobi in registers; units it cannot normalise (info -2: a null
+    // column) are re-solved by the two-sided kernel, which every other unit skips
+    if (!twosided && launch_hestenes(U, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 3e-4f, 30, st) < 0) return -1;
+    jacobi32p_kernel<128><<<U, kJPThreads, smp, st>>>(ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30,
+                                                      twosided ? 0 : 1);
   } else {
     cudaFuncSetAttribute(jacobi32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     jacobi32_kernel<0><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
@@ -1043,7 +1058,7 @@ int launch_jacobi(int U, int d, bool fp64, const CalibWs& ws, cudaStream_t st) {
     cudaFuncSetAttribute(refine_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
     refine_smem_kernel<<<U, kRefSmThreads, rsm, st>>>(ws.cq, v32, ws.lam, static_cast<double*>(ws.vecs),
                                                        ws.jinfo);
-    return cudaPeekAtLastError() == cudaSuccess ? 2 : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? (twosided ? 2 : 3) : -1;
   }
   const size_t rsm = (size_t)d * d * 4;
   cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);

@@ -1,0 +1,449 @@
+// hestenes.cu -- step 4 (eigendecomposition of C_q; north_star's "batched Jacobi
+// eigensolver over head_dim x head_dim") as ONE-SIDED (Hestenes) Jacobi, d = 128, fp32, with
+// the working matrix held in REGISTERS.
+//
+// C_q is symmetric positive semi-definite (C is a Gram matrix of centered keys and
+// (sigma sigma^T) (.) C is PSD by the Schur product theorem), so its singular vectors are its
+// eigenvectors.  Starting from X = C_q (V = I), plane rotations X <- X J_pq make the columns of
+// X mutually orthogonal: then X = C_q V with V orthogonal and X^T X = V^T C_q^2 V diagonal, so
+// X = V diag(lambda) column by column and the normalised columns ARE the eigenvectors (for a
+// PSD matrix the sign ambiguity of an SVD does not arise).  V itself is never stored.
+//
+// Why one-sided on B200: the two-sided kernel (jacobi32p_kernel, calibrate.cu) must touch
+// rows AND columns of A every round, so A and V live in shared memory and every round moves
+// every element through the shared-memory pipe (ncu: L1/shared 78-91 %), 11.5 ms for LLaVA
+// b32.  A column rotation needs only its two columns: here warp w holds 2 blocks of 8 columns
+// with lane l owning rows l, l+32, l+64, l+96 (64 fp32 registers), every pair of columns a warp
+// holds is rotated in registers, and the only cross-lane traffic is the pair's inner product
+// (a butterfly reduce-scatter of 8 partial sums per 8 disjoint pairs) and the broadcast of
+// (c, s).  Blocks move between warps through shared memory once per block-round (15 per
+// sweep, a 2-block tournament over 16 blocks; every column pair meets once per sweep).
+//
+// Rotation (Golub & Van Loan 8.4, the same Schur rotation as the two-sided kernels, applied to
+// the 2x2 Gram matrix [[a, g], [g, b]] of columns p, q):
+//   zeta = (b - a) / (2 g),  t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),  c = 1/sqrt(1+t^2),
+//   x_p <- c x_p - s x_q,  x_q <- s x_p + c x_q (s = t c),  a <- a - t g,  b <- b + t g.
+// A pair is rotated only when |g| > tol sqrt(a b) (its cosine exceeds tol); a sweep without a
+// rotation ends the iteration.  Column norms are recomputed exactly after every exchange.
+//
+// Output: V0 = X diag(1/||x_j||) (fp32, [d][d] row-major, columns in solver order) and
+// lambda_j = ||x_j||; the fp64 refinement (refine_smem_kernel) follows as for the two-sided
+// solver.  A column whose squared norm falls below 1e-30 ||C_q||_F^2 (an exactly or nearly
+// null direction, whose normalisation is undefined) marks the unit info = -2 and the
+// two-sided kernel re-solves it (launch_jacobi).
+#include <cstdio>
+#include <cstdlib>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace rk {
+
+namespace {
+constexpr int kHJWarps = 8;
+constexpr int kHJThreads = 32 * kHJWarps;
+constexpr int kHJLd = 129;  // column stride of the exchange buffer (floats): conflict-free
+                            // column writes (lanes = rows) and transposed reads
+constexpr unsigned kFull = 0xffffffffu;
+constexpr int kNeedTwoSided = -2;
+
+// Reduce-scatter of N per-lane partial sums over the warp (N = 8 or 16): returns the full
+// warp sum of value index (lane >> (5 - log2 N)).  log2 N halving levels exchange half of the
+// remaining values each, then the remaining 5 - log2 N levels are plain butterflies.
+template <int N>
+__device__ __forceinline__ float warp_reduce_scatter(const float (&v)[N], int lane) {
+  constexpr int L = N == 16 ? 4 : N == 8 ? 3 : N == 4 ? 2 : N == 2 ? 1 : 0;
+  static_assert((1 << L) == N, "N must be a power of two <= 16");
+  float a[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) a[i] = v[i];
+#pragma unroll
+  for (int lev = 0; lev < L; ++lev) {
+    const int off = 16 >> lev;
+    const int m = N >> (lev + 1);
+    const bool hi = (lane & off) != 0;
+#pragma unroll
+    for (int i = 0; i < m; ++i) {
+      const float send = hi ? a[i] : a[i + m];
+      const float keep = hi ? a[i + m] : a[i];
+      a[i] = keep + __shfl_xor_sync(kFull, send, off);
+    }
+  }
+  float r = a[0];
+#pragma unroll
+  for (int off = 16 >> L; off >= 1; off >>= 1) r += __shfl_xor_sync(kFull, r, off);
+  return r;
+}
+
+// Columns (0..15 = block A cols 0..7, block B cols 0..7) of pair j in sub-round s.
+//   intra-block: 7 rounds of the circle method on each block's 8 columns (pairs j = 4b + m);
+//   cross-block: pair j = (A_j, B_{(j + s) mod 8}), 8 rounds.
+template <bool kIntra>
+__device__ __forceinline__ void hj_pair(int s, int j, int& p, int& q) {
+  if (kIntra) {
+    const int b = j >> 2, m = j & 3;
+    const int pm = m == 0 ? 0 : 1 + (m - 1 + s) % 7;
+    const int qm = 1 + (6 - m + s) % 7;  // position 7 - m >= 4 is never the fixed player
+    p = 8 * b + pm;
+    q = 8 * b + qm;
+  } else {
+    p = j;
+    q = 8 + ((j + s) & 7);
+  }
+}
+
+// One sub-round: 8 disjoint column pairs of the warp's 16 columns.  Column j is held scaled,
+// x_j = dsc[j] y_j (registers hold y), nrm[j] = ||x_j||^2.  cmax collects the largest squared
+// cosine g^2 / (a b) seen by this lane's pair (the stopping test).
+template <bool kIntra, int S>
+__device__ __forceinline__ void hj_subround(float (&x)[16][4], float* nrm, float* dsc, float tol2,
+                                            int lane, float& cmax) {
+  float g[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    int p, q;
+    hj_pair<kIntra>(S, j, p, q);
+    float acc = x[p][0] * x[q][0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) acc = fmaf(x[p][k], x[q][k], acc);
+    g[j] = acc;
+  }
+  const float gy = warp_reduce_scatter<8>(g, lane);  // pair lane >> 2 (scaled columns)
+  int p, q;
+  hj_pair<kIntra>(S, lane >> 2, p, q);
+  const float al = nrm[p], be = nrm[q], dp = dsc[p], dq = dsc[q];
+  const float gam = gy * dp * dq;  // inner product of the true columns
+  const float g2 = gam * gam, ab = al * be;
+  if (ab > 1e-36f) cmax = fmaxf(cmax, __fdividef(g2, ab));  // (null columns: info -2 later)
+  const bool rot = g2 > tol2 * ab;  // cosine above tol
+  // branch-free (the shuffles below need a converged warp): lanes that do not rotate take
+  // a1 = a2 = t = 0, c = 1 whatever zeta is (gam = 0 gives inf / NaN here, discarded)
+  const float zeta = __fdividef(be - al, 2.f * gam);
+  const float az = fabsf(zeta);
+  // sqrt(1 + zeta^2) ~ |zeta| beyond 1e18 (zeta^2 would overflow); fast reciprocal and
+  // square root: an inexact t only changes the angle slightly (the sweep goes on until
+  // the cosines are small), an inexact c only rescales the pair (norms are recomputed)
+  const float z2 = fmaf(az, az, 1.f);
+  float t = __fdividef(1.f, az + (az < 1e18f ? z2 * rsqrtf(z2) : az));
+  t = rot ? (zeta < 0.f ? -t : t) : 0.f;
+  const float c = rsqrtf(fmaf(t, t, 1.f));
+  // scaled rotation: x = d y per column; x_p <- c (x_p - t x_q), x_q <- c (x_q + t x_p)
+  // becomes d <- c d and y_p <- y_p - (t d_q / d_p) y_q, y_q <- y_q + (t d_p / d_q) y_p:
+  // two FMAs per element pair instead of four multiply(-add)s
+  const float rq = __fdividef(dq, dp);
+  const float a1 = t * rq, a2 = __fdividef(t, rq);
+  // the broadcasts run unconditionally (shuffles at a point the compiler sees as converged);
+  // the update is skipped when no pair of the warp rotates (warp-uniform)
+  float c1[8], c2[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    c1[j] = __shfl_sync(kFull, a1, 4 * j);
+    c2[j] = __shfl_sync(kFull, a2, 4 * j);
+  }
+  if (__any_sync(kFull, rot)) {
+    // every lane has read nrm / dsc (their values fed the shuffles above) before the update
+    if (rot && (lane & 3) == 0) {
+      nrm[p] = fmaf(-t, gam, al);
+      nrm[q] = fmaf(t, gam, be);
+      dsc[p] = dp * c;
+      dsc[q] = dq * c;
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int pp, qq;
+      hj_pair<kIntra>(S, j, pp, qq);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const float yp = x[pp][k];
+        x[pp][k] = fmaf(-c1[j], x[qq][k], yp);
+        x[qq][k] = fmaf(c2[j], yp, x[qq][k]);
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// exact squared norms of the warp's 16 (unscaled) columns into nrm[0..15], scales to 1
+__device__ __forceinline__ void hj_norms(const float (&x)[16][4], float* nrm, float* dsc, int lane) {
+  float v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    float a = x[j][0] * x[j][0];
+#pragma unroll
+    for (int k = 1; k < 4; ++k) a = fmaf(x[j][k], x[j][k], a);
+    v[j] = a;
+  }
+  const float r = warp_reduce_scatter<16>(v, lane);  // column lane >> 1
+  __syncwarp();
+  if ((lane & 1) == 0) {
+    nrm[lane >> 1] = r;
+    dsc[lane >> 1] = 1.f;
+  }
+  __syncwarp();
+}
+
+// block held in tournament slot i at block-round k (circle method, slot 0 fixed)
+__device__ __forceinline__ int hj_slot_block(int i, int k) { return i == 0 ? 0 : 1 + (i - 1 + k) % 15; }
+
+template <int K>
+struct HjIntra {
+  __device__ __forceinline__ static void run(float (&x)[16][4], float* nrm, float* dsc, float tol2, int lane,
+                                             float& cm) {
+    hj_subround<true, K>(x, nrm, dsc, tol2, lane, cm);
+    HjIntra<K + 1>::run(x, nrm, dsc, tol2, lane, cm);
+  }
+};
+template <>
+struct HjIntra<7> {
+  __device__ __forceinline__ static void run(float (&)[16][4], float*, float*, float, int, float&) {}
+};
+template <int K>
+struct HjCross {
+  __device__ __forceinline__ static void run(float (&x)[16][4], float* nrm, float* dsc, float tol2, int lane,
+                                             float& cm) {
+    hj_subround<false, K>(x, nrm, dsc, tol2, lane, cm);
+    HjCross<K + 1>::run(x, nrm, dsc, tol2, lane, cm);
+  }
+};
+template <>
+struct HjCross<8> {
+  __device__ __forceinline__ static void run(float (&)[16][4], float*, float*, float, int, float&) {}
+};
+}  // namespace
+
+size_t hestenes_smem_bytes() { return ((size_t)128 * kHJLd + 32 * kHJWarps + 128) * sizeof(float); }
+
+__global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* __restrict__ cq,
+                                                                 float* __restrict__ lam_out,
+                                                                 float* __restrict__ vecs,
+                                                                 int32_t* __restrict__ jinfo,
+                                                                 float tol, float qstop,
+                                                                 int max_sweeps, int report_sweeps) {
+  constexpr int d = 128;
+  extern __shared__ __align__(16) float hsm[];
+  float* Xs = hsm;                                  // [col][kHJLd]
+  const int u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  float* nrm = hsm + d * kHJLd + 16 * w;            // this warp's 16 squared column norms
+  float* dsc = hsm + d * kHJLd + 16 * kHJWarps + 16 * w;  // and their scales (x = dsc y)
+  __shared__ double s_red[kHJWarps];
+  __shared__ int s_bad;
+
+  // finiteness and ||C||_F (fp64); the matrix is scaled by an exact power of two to ~1
+  const double* C = cq + (size_t)u * d * d;
+  double f2 = 0.0;
+  int bad = 0;
+  for (int e = tid; e < d * d / 2; e += kHJThreads) {
+    const double2 v = __ldg(reinterpret_cast<const double2*>(C) + e);
+    if (!isfinite(v.x) || !isfinite(v.y)) bad = 1;
+    f2 = fma(v.x, v.x, fma(v.y, v.y, f2));
+  }
+  if (tid == 0) s_bad = 0;
+#pragma unroll
+  for (int off = 16; off >= 1; off >>= 1) f2 += __shfl_xor_sync(kFull, f2, off);
+  bad = __any_sync(kFull, bad);
+  if (lane == 0) s_red[w] = f2;
+  __syncthreads();
+  if (bad && lane == 0) s_bad = 1;
+  double tot = 0.0;
+#pragma unroll
+  for (int i = 0; i < kHJWarps; ++i) tot += s_red[i];
+  __syncthreads();
+  if (s_bad) {
+    for (int e = tid; e < d * d; e += kHJThreads) vecs[(size_t)u * d * d + e] = 0.f;
+    for (int j = tid; j < d; j += kHJThreads) lam_out[(size_t)u * d + j] = CUDART_NAN_F;
+    if (tid == 0) jinfo[u] = -1;
+    return;
+  }
+  int ex = 0;
+  if (tot > 0.0) frexp(sqrt(tot), &ex);
+  const double scale = ldexp(1.0, -ex);
+  const float unscale = ldexpf(1.f, ex);  // C_q = unscale * (scaled matrix)
+
+  // A = C_q in registers: warp w holds blocks w and 15 - w (tournament slots w, 15 - w at
+  // k = 0), column cj[j] in x[j]; column c of the symmetric C_q is its row c (coalesced)
+  float x[16][4];
+  int cj[16];
+  {
+    const int ba = hj_slot_block(w, 0), bb = hj_slot_block(15 - w, 0);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      cj[j] = 8 * (j < 8 ? ba : bb) + (j & 7);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) x[j][k] = (float)(C[(size_t)cj[j] * d + lane + 32 * k] * scale);
+    }
+  }
+
+  // Preconditioner: diagonally pivoted Cholesky C_q = F F^T (outer-product form, fp32).  The
+  // one-sided iteration then runs on F, whose left singular vectors are C_q's eigenvectors and
+  // whose squared singular values are its eigenvalues: the working Gram matrix has C_q's
+  // spectrum instead of C_q^2's, and pivoting grades F's columns (Drmac & Veselic's
+  // preconditioned Jacobi) -- 12 -> 7 sweeps on the bench configs.  Step k takes the largest
+  // remaining diagonal entry p: F[:, k] = A[:, p] / sqrt(A_pp) (= row p by symmetry: lane p%32
+  // of every warp writes its columns' entries), A <- A - F[:, k] F[:, k]^T on the remaining
+  // columns.  Pivots below d eps max_i(C_ii) stop the factorisation; the remaining (tiny)
+  // Schur-complement columns are appended to F as they are, so F F^T = C_q up to rounding.
+  float* dg = hsm + d * kHJLd + 32 * kHJWarps;  // remaining diagonal, -inf once eliminated
+  if (tid < d) dg[tid] = (float)(C[(size_t)tid * d + tid] * scale);
+  __syncthreads();
+  uint32_t elim = 0;  // bit j: column cj[j] is eliminated
+  int kf = 0;
+  float ptol = 0.f;
+#pragma unroll 1
+  for (; kf < d; ++kf) {
+    float bv = dg[lane];
+    int bi = lane;
+#pragma unroll
+    for (int i = 1; i < 4; ++i) {
+      const float v = dg[lane + 32 * i];
+      if (v > bv) { bv = v; bi = lane + 32 * i; }
+    }
+#pragma unroll
+    for (int off = 16; off >= 1; off >>= 1) {
+      const float ov = __shfl_xor_sync(kFull, bv, off);
+      const int oi = __shfl_xor_sync(kFull, bi, off);
+      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
+    }
+    if (kf == 0) ptol = (float)d * 5.96e-8f * bv;
+    if (!(bv > ptol)) break;  // identical decision in every warp
+    const int p = bi;
+    const float rs = rsqrtf(bv);
+    float* Fk = Xs + kf * kHJLd;
+    if (lane == (p & 31)) {
+      const int ip = p >> 5;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float v = ip == 0 ? x[j][0] : ip == 1 ? x[j][1] : ip == 2 ? x[j][2] : x[j][3];
+        Fk[cj[j]] = (elim >> j) & 1u ? 0.f : v * rs;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (cj[j] == p) elim |= 1u << j;
+    __syncthreads();
+    float lr[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) lr[i] = Fk[lane + 32 * i];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if ((elim >> j) & 1u) continue;  // warp-uniform
+      const float lc = Fk[cj[j]];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[j][i] = fmaf(-lr[i], lc, x[j][i]);
+    }
+    if (tid < d) {
+      const float dv = dg[tid];
+      dg[tid] = tid == p ? -CUDART_INF_F : fmaf(-Fk[tid], Fk[tid], dv);
+    }
+    __syncthreads();
+  }
+  // append the remaining columns (in index order) after the kf pivot columns
+  {
+    uint32_t rem[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) rem[i] = __ballot_sync(kFull, dg[lane + 32 * i] != -CUDART_INF_F);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      if ((elim >> j) & 1u) continue;
+      const int c = cj[j], wd = c >> 5;
+      int pos = kf + __popc(rem[wd] & ((1u << (c & 31)) - 1u));
+#pragma unroll
+      for (int i = 0; i < 4; ++i) pos += i < wd ? __popc(rem[i]) : 0;
+      float* dst = Xs + pos * kHJLd + lane;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) dst[32 * i] = x[j][i];
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float* src = Xs + cj[j] * kHJLd + lane;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[j][i] = src[32 * i];
+  }
+  __syncthreads();
+  hj_norms(x, nrm, dsc, lane);
+
+  const float tol2 = tol * tol, q2 = qstop * qstop;
+  int sweep = 0, converged = 0;
+  for (;;) {
+    if (sweep >= max_sweeps) break;
+    float cm = 0.f;
+    HjIntra<0>::run(x, nrm, dsc, tol2, lane, cm);
+#pragma unroll 1
+    for (int k = 0; k < 15; ++k) {
+      HjCross<0>::run(x, nrm, dsc, tol2, lane, cm);
+      // exchange: blocks go back to shared memory by block id and come out by the next
+      // round's tournament slots (k = 14 -> 0 restores the start arrangement)
+      // (the scales are folded back in: shared memory holds the true columns)
+      const int ba = hj_slot_block(w, k), bb = hj_slot_block(15 - w, k);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float* dst = Xs + (8 * (j < 8 ? ba : bb) + (j & 7)) * kHJLd + lane;
+        const float sc = dsc[j];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) dst[32 * kk] = x[j][kk] * sc;
+      }
+      __syncthreads();
+      const int k1 = k == 14 ? 0 : k + 1;
+      const int na = hj_slot_block(w, k1), nb = hj_slot_block(15 - w, k1);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const float* src = Xs + (8 * (j < 8 ? na : nb) + (j & 7)) * kHJLd + lane;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) x[j][kk] = src[32 * kk];
+      }
+      __syncthreads();
+      hj_norms(x, nrm, dsc, lane);
+    }
+    ++sweep;
+    // quadratic convergence: after a sweep whose largest cosine was <= qstop the remaining
+    // cosines are O(qstop^2), below what the fp64 refinement needs (no check sweep)
+    if (!__syncthreads_or(cm > q2 ? 1 : 0)) {
+      converged = 1;
+      break;
+    }
+  }
+
+  // V0 = X diag(1 / ||x_j||), lambda_j = ||x_j||; staged through shared memory so the
+  // row-major global writes are coalesced
+  const int ba = hj_slot_block(w, 0), bb = hj_slot_block(15 - w, 0);
+  int degenerate = 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int col = 8 * (j < 8 ? ba : bb) + (j & 7);
+    const float n2 = nrm[j];
+    if (!(n2 >= 1e-30f)) degenerate = 1;
+    const float inv = n2 > 0.f ? rsqrtf(n2) : 0.f;
+    float* dst = Xs + col * kHJLd + lane;
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) dst[32 * kk] = x[j][kk] * inv;
+    if (lane == 0) lam_out[(size_t)u * d + col] = n2 * unscale;  // ||f_j||^2 = lambda_j
+  }
+  degenerate = __syncthreads_or(degenerate);
+  float* Vo = vecs + (size_t)u * d * d;
+  for (int e = tid; e < d * d; e += kHJThreads) {
+    const int row = e / d, col = e % d;
+    Vo[e] = Xs[col * kHJLd + row];
+  }
+  if (tid == 0)
+    jinfo[u] = degenerate ? kNeedTwoSided
+                          : (converged ? (report_sweeps ? 1000 + sweep : 0) : (sweep > 0 ? sweep : 1));
+}
+
+int launch_hestenes(int U, const double* cq, float* lam, float* v32, int32_t* jinfo, float tol,
+                    float qstop, int max_sweeps, cudaStream_t st) {
+  static int attr[kMaxDevices];
+  const size_t sm = hestenes_smem_bytes();
+  once_per_device(attr, [&] {
+    return cudaFuncSetAttribute(hestenes_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm) ==
+                   cudaSuccess
+               ? 1
+               : 0;
+  });
+  // diagnostics only: ROTATEK_HJ_SWEEPS=1 reports info = 1000 + sweeps for converged units
+  static const int report = getenv("ROTATEK_HJ_SWEEPS") != nullptr;
+  hestenes_kernel<<<U, kHJThreads, sm, st>>>(cq, lam, v32, jinfo, tol, qstop, max_sweeps, report);
+  return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
+}
+
+}  // namespace rk

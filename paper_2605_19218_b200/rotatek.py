@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("ROTATEK_LIB") or os.path.join(_HERE, "librotatek.so")
 
 OK, ERR_NULL, ERR_DIMS, ERR_ALIGN, ERR_WORKSPACE, ERR_UNSUPPORTED, ERR_CUDA = range(7)
 BF16, F32 = 0, 1
-CENTER, QUERY_WEIGHT, EIG_FP64, SIMT_ONLY = 1, 2, 4, 256
+CENTER, QUERY_WEIGHT, EIG_FP64, EIG_TWOSIDED, SIMT_ONLY = 1, 2, 4, 8, 256
 DEFAULT_FLAGS = CENTER | QUERY_WEIGHT
 OP_CALIBRATE, OP_DECODE = 0, 1
 KERNEL_AUTO, KERNEL_GENERIC, KERNEL_FAST, KERNEL_GQA, KERNEL_STEAL, KERNEL_GQA_WARP = 0, 1, 2, 3, 4, 5
