@@ -132,7 +132,11 @@ size_t rotatek_workspace_bytes(const rotatek_dims* dims, rotatek_op op);
  *            select step ranks exactly these fp32 values.
  *   keep_mask[U, ceil(d/32)] uint32, bit i%32 of word i/32 <=> channel i kept (nullable)
  *   keep_idx [U, r] int32 ascending (nullable)
- *   R_full   [U, d, d] fp32 full eigenbasis, columns in solver order (nullable; tests)
+ *   R_full   [U, d, d] fp32 full eigenbasis, columns in solver order (nullable; tests).
+ *            Default solver (d = 128, r <= 64): the r + 8 leading columns carry the fp64
+ *            refinement, the others the one-sided solver's basis (orthonormal to ~1e-7;
+ *            ~1e-4 per entry for a unit re-solved by the two-sided kernel after a null
+ *            C_q column)
  *   info     [U] int32: 0 ok; s > 0 not converged after s sweeps (results are
  *            still written); -1 non-finite input (R, dmu zero-filled, mask 0,
  *            idx -1) (nullable)

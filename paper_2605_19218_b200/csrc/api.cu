@@ -120,7 +120,7 @@ rotatek_status calibrate_impl(const rotatek_dims* dm, uint32_t flags, const void
     return s;
   if (!(tc && ws.parts == 1))  // the tensor-core kernel finalizes in place when one CTA sees the unit
     if ((s = launched(rk::launch_finalize(U, N, d, center, ws, st, tsrc.nvu), &n))) return s;
-  if ((s = launched(rk::launch_jacobi(U, d, fp64, (flags & ROTATEK_EIG_TWOSIDED) != 0, ws, st), &n))) return s;
+  if ((s = launched(rk::launch_jacobi(U, d, r, fp64, (flags & ROTATEK_EIG_TWOSIDED) != 0, ws, st), &n))) return s;
   if ((s = launched(rk::launch_select_gather(U, d, r, /*fp64_vecs=*/true, bf16, center, ws, R, dmu, eigvals,
                                              keep_mask, keep_idx, R_full, info, st), &n)))
     return s;
@@ -251,7 +251,7 @@ rotatek_status rotatek_calibrate_from_state(const rotatek_dims* dm, uint32_t fla
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   int n = 0;
   if ((s = launched(rk::launch_state_finalize(U, d, center, weight, state, ws, st), &n))) return s;
-  if ((s = launched(rk::launch_jacobi(U, d, fp64, (flags & ROTATEK_EIG_TWOSIDED) != 0, ws, st), &n))) return s;
+  if ((s = launched(rk::launch_jacobi(U, d, r, fp64, (flags & ROTATEK_EIG_TWOSIDED) != 0, ws, st), &n))) return s;
   if ((s = launched(rk::launch_select_gather(U, d, r, /*fp64_vecs=*/true, bf16, center, ws, R, dmu, eigvals,
                                              keep_mask, keep_idx, R_full, info, st), &n)))
     return s;

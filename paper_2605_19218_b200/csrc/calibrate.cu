@@ -1028,7 +1028,11 @@ __global__ void __launch_bounds__(kRefSmThreads, 1) refine_smem_kernel(const dou
 int launch_hestenes(int U, const double* cq, float* lam, float* v32, int32_t* jinfo, float tol,
                     float qstop, int max_sweeps, cudaStream_t st);
 
-int launch_jacobi(int U, int d, bool fp64, bool twosided, const CalibWs& ws, cudaStream_t st) {
+int refine_tc_candidates(int d, int r);
+int launch_refine_tc(int U, int kc, const double* cq, const float* v32, float* lam, double* vecs,
+                     const int32_t* jinfo, cudaStream_t st);
+
+int launch_jacobi(int U, int d, int r, bool fp64, bool twosided, const CalibWs& ws, cudaStream_t st) {
   if (fp64) {
     size_t sm = jacobi_smem_bytes(d, true);
     cudaFuncSetAttribute(jacobi_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1045,7 +1049,7 @@ int launch_jacobi(int U, int d, bool fp64, bool twosided, const CalibWs& ws, cud
     cudaFuncSetAttribute(jacobi32p_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
     // default: one-sided Jacobi in registers; units it cannot normalise (info -2: a null
     // column) are re-solved by the two-sided kernel, which every other unit skips
-    if (!twosided && launch_hestenes(U, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 3e-4f, 30, st) < 0) return -1;
+    if (!twosided && launch_hestenes(U, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 1e-3f, 30, st) < 0) return -1;
     jacobi32p_kernel<128><<<U, kJPThreads, smp, st>>>(ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30,
                                                       twosided ? 0 : 1);
   } else {
@@ -1053,12 +1057,22 @@ int launch_jacobi(int U, int d, bool fp64, bool twosided, const CalibWs& ws, cud
     jacobi32_kernel<0><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return -1;
+  // fp64 refinement: on the fp64 tensor cores for the r + 8 leading columns (refine_tc.cu)
+  // when r <= 64 behind the one-sided solver (whose other columns are orthonormal to ~1e-7
+  // as they are), else every column on CUDA cores (the two-sided solver's fp32 basis is
+  // orthonormal only to ~1e-4 per entry: R_full needs the full step)
+  const int launches = twosided ? 2 : 3;
+  if (const int kc = twosided ? 0 : refine_tc_candidates(d, r)) {
+    if (launch_refine_tc(U, kc, ws.cq, v32, ws.lam, static_cast<double*>(ws.vecs), ws.jinfo, st) < 0)
+      return -1;
+    return launches;
+  }
   if (d == 128) {
     const size_t rsm = (size_t)d * d * (8 + 4);
     cudaFuncSetAttribute(refine_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);
     refine_smem_kernel<<<U, kRefSmThreads, rsm, st>>>(ws.cq, v32, ws.lam, static_cast<double*>(ws.vecs),
                                                        ws.jinfo);
-    return cudaPeekAtLastError() == cudaSuccess ? (twosided ? 2 : 3) : -1;
+    return cudaPeekAtLastError() == cudaSuccess ? launches : -1;
   }
   const size_t rsm = (size_t)d * d * 4;
   cudaFuncSetAttribute(refine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm);

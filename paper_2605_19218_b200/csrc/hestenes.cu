@@ -96,17 +96,15 @@ __device__ __forceinline__ void hj_pair(int s, int j, int& p, int& q) {
 // x_j = dsc[j] y_j (registers hold y), nrm[j] = ||x_j||^2.  cmax collects the largest squared
 // cosine g^2 / (a b) seen by this lane's pair (the stopping test).
 template <bool kIntra, int S>
-__device__ __forceinline__ void hj_subround(float (&x)[16][4], float* nrm, float* dsc, float tol2,
+__device__ __forceinline__ void hj_subround(float2 (&x)[16][2], float* nrm, float* dsc, float tol2,
                                             int lane, float& cmax) {
   float g[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
     int p, q;
     hj_pair<kIntra>(S, j, p, q);
-    float acc = x[p][0] * x[q][0];
-#pragma unroll
-    for (int k = 1; k < 4; ++k) acc = fmaf(x[p][k], x[q][k], acc);
-    g[j] = acc;
+    const float2 a2 = __ffma2_rn(x[p][1], x[q][1], __fmul2_rn(x[p][0], x[q][0]));
+    g[j] = a2.x + a2.y;
   }
   const float gy = warp_reduce_scatter<8>(g, lane);  // pair lane >> 2 (scaled columns)
   int p, q;
@@ -132,16 +130,8 @@ __device__ __forceinline__ void hj_subround(float (&x)[16][4], float* nrm, float
   // two FMAs per element pair instead of four multiply(-add)s
   const float rq = __fdividef(dq, dp);
   const float a1 = t * rq, a2 = __fdividef(t, rq);
-  // the broadcasts run unconditionally (shuffles at a point the compiler sees as converged);
-  // the update is skipped when no pair of the warp rotates (warp-uniform)
-  float c1[8], c2[8];
-#pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    c1[j] = __shfl_sync(kFull, a1, 4 * j);
-    c2[j] = __shfl_sync(kFull, a2, 4 * j);
-  }
-  if (__any_sync(kFull, rot)) {
-    // every lane has read nrm / dsc (their values fed the shuffles above) before the update
+  if (__any_sync(kFull, rot)) {  // warp-uniform: skip the update when no pair rotates
+    // every lane has read nrm / dsc (their values fed the vote above) before the update
     if (rot && (lane & 3) == 0) {
       nrm[p] = fmaf(-t, gam, al);
       nrm[q] = fmaf(t, gam, be);
@@ -149,14 +139,16 @@ __device__ __forceinline__ void hj_subround(float (&x)[16][4], float* nrm, float
       dsc[q] = dq * c;
     }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {
+    for (int j = 0; j < 8; ++j) {  // pair j's coefficients from its lane group, then its update
       int pp, qq;
       hj_pair<kIntra>(S, j, pp, qq);
+      const float c1 = __shfl_sync(kFull, a1, 4 * j), c2 = __shfl_sync(kFull, a2, 4 * j);
+      const float2 m1 = make_float2(-c1, -c1), m2 = make_float2(c2, c2);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const float yp = x[pp][k];
-        x[pp][k] = fmaf(-c1[j], x[qq][k], yp);
-        x[qq][k] = fmaf(c2[j], yp, x[qq][k]);
+      for (int h = 0; h < 2; ++h) {  // packed fp32x2 FMAs (FFMA2): two rows per instruction
+        const float2 yp = x[pp][h];
+        x[pp][h] = __ffma2_rn(m1, x[qq][h], yp);
+        x[qq][h] = __ffma2_rn(m2, yp, x[qq][h]);
       }
     }
   }
@@ -164,14 +156,12 @@ __device__ __forceinline__ void hj_subround(float (&x)[16][4], float* nrm, float
 }
 
 // exact squared norms of the warp's 16 (unscaled) columns into nrm[0..15], scales to 1
-__device__ __forceinline__ void hj_norms(const float (&x)[16][4], float* nrm, float* dsc, int lane) {
+__device__ __forceinline__ void hj_norms(const float2 (&x)[16][2], float* nrm, float* dsc, int lane) {
   float v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    float a = x[j][0] * x[j][0];
-#pragma unroll
-    for (int k = 1; k < 4; ++k) a = fmaf(x[j][k], x[j][k], a);
-    v[j] = a;
+    const float2 a = __ffma2_rn(x[j][1], x[j][1], __fmul2_rn(x[j][0], x[j][0]));
+    v[j] = a.x + a.y;
   }
   const float r = warp_reduce_scatter<16>(v, lane);  // column lane >> 1
   __syncwarp();
@@ -182,12 +172,18 @@ __device__ __forceinline__ void hj_norms(const float (&x)[16][4], float* nrm, fl
   __syncwarp();
 }
 
+// element k (row lane + 32 k) of column j: rows (lane, lane + 32) and (lane + 64, lane + 96)
+// are packed in one float2 each so the rotations run as FFMA2
+__device__ __forceinline__ float& xel(float2 (&x)[16][2], int j, int k) {
+  return (k & 1) ? x[j][k >> 1].y : x[j][k >> 1].x;
+}
+
 // block held in tournament slot i at block-round k (circle method, slot 0 fixed)
 __device__ __forceinline__ int hj_slot_block(int i, int k) { return i == 0 ? 0 : 1 + (i - 1 + k) % 15; }
 
 template <int K>
 struct HjIntra {
-  __device__ __forceinline__ static void run(float (&x)[16][4], float* nrm, float* dsc, float tol2, int lane,
+  __device__ __forceinline__ static void run(float2 (&x)[16][2], float* nrm, float* dsc, float tol2, int lane,
                                              float& cm) {
     hj_subround<true, K>(x, nrm, dsc, tol2, lane, cm);
     HjIntra<K + 1>::run(x, nrm, dsc, tol2, lane, cm);
@@ -195,11 +191,11 @@ struct HjIntra {
 };
 template <>
 struct HjIntra<7> {
-  __device__ __forceinline__ static void run(float (&)[16][4], float*, float*, float, int, float&) {}
+  __device__ __forceinline__ static void run(float2 (&)[16][2], float*, float*, float, int, float&) {}
 };
 template <int K>
 struct HjCross {
-  __device__ __forceinline__ static void run(float (&x)[16][4], float* nrm, float* dsc, float tol2, int lane,
+  __device__ __forceinline__ static void run(float2 (&x)[16][2], float* nrm, float* dsc, float tol2, int lane,
                                              float& cm) {
     hj_subround<false, K>(x, nrm, dsc, tol2, lane, cm);
     HjCross<K + 1>::run(x, nrm, dsc, tol2, lane, cm);
@@ -207,11 +203,11 @@ struct HjCross {
 };
 template <>
 struct HjCross<8> {
-  __device__ __forceinline__ static void run(float (&)[16][4], float*, float*, float, int, float&) {}
+  __device__ __forceinline__ static void run(float2 (&)[16][2], float*, float*, float, int, float&) {}
 };
 }  // namespace
 
-size_t hestenes_smem_bytes() { return ((size_t)128 * kHJLd + 32 * kHJWarps + 128) * sizeof(float); }
+size_t hestenes_smem_bytes() { return ((size_t)128 * kHJLd + 32 * kHJWarps) * sizeof(float); }
 
 __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* __restrict__ cq,
                                                                  float* __restrict__ lam_out,
@@ -260,18 +256,14 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
   const float unscale = ldexpf(1.f, ex);  // C_q = unscale * (scaled matrix)
 
   // A = C_q in registers: warp w holds blocks w and 15 - w (tournament slots w, 15 - w at
-  // k = 0), column cj[j] in x[j]; column c of the symmetric C_q is its row c (coalesced)
-  float x[16][4];
-  int cj[16];
-  {
-    const int ba = hj_slot_block(w, 0), bb = hj_slot_block(15 - w, 0);
+  // k = 0), column cj(j) in x[j]; column c of the symmetric C_q is its row c (coalesced)
+  float2 x[16][2];
+  // blocks w and 15 - w: column of x[j] (computed, not held: registers are the budget)
+  auto cj = [w](int j) { return j < 8 ? 8 * w + j : 112 - 8 * w + j; };
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      cj[j] = 8 * (j < 8 ? ba : bb) + (j & 7);
+  for (int j = 0; j < 16; ++j)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) x[j][k] = (float)(C[(size_t)cj[j] * d + lane + 32 * k] * scale);
-    }
-  }
+    for (int k = 0; k < 4; ++k) xel(x, j, k) = (float)(C[(size_t)cj(j) * d + lane + 32 * k] * scale);
 
   // Preconditioner: diagonally pivoted Cholesky C_q = F F^T (outer-product form, fp32).  The
   // one-sided iteration then runs on F, whose left singular vectors are C_q's eigenvectors and
@@ -282,83 +274,80 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
   // of every warp writes its columns' entries), A <- A - F[:, k] F[:, k]^T on the remaining
   // columns.  Pivots below d eps max_i(C_ii) stop the factorisation; the remaining (tiny)
   // Schur-complement columns are appended to F as they are, so F F^T = C_q up to rounding.
-  float* dg = hsm + d * kHJLd + 32 * kHJWarps;  // remaining diagonal, -inf once eliminated
-  if (tid < d) dg[tid] = (float)(C[(size_t)tid * d + tid] * scale);
-  __syncthreads();
-  uint32_t elim = 0;  // bit j: column cj[j] is eliminated
+  // The remaining diagonal is tracked in registers, redundantly by every warp (lane l holds
+  // rows l + 32 i), so a step needs a single barrier: the pivot column's publication.
+  float dgr[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) dgr[i] = (float)(C[(size_t)(lane + 32 * i) * (d + 1)] * scale);
+  uint32_t elim = 0;  // bit j: column cj(j) is eliminated
   int kf = 0;
   float ptol = 0.f;
 #pragma unroll 1
   for (; kf < d; ++kf) {
-    float bv = dg[lane];
+    // pivot: largest remaining diagonal entry, ties -> lowest index (eliminated: -inf)
+    float bv = dgr[0];
     int bi = lane;
 #pragma unroll
-    for (int i = 1; i < 4; ++i) {
-      const float v = dg[lane + 32 * i];
-      if (v > bv) { bv = v; bi = lane + 32 * i; }
-    }
-#pragma unroll
-    for (int off = 16; off >= 1; off >>= 1) {
-      const float ov = __shfl_xor_sync(kFull, bv, off);
-      const int oi = __shfl_xor_sync(kFull, bi, off);
-      if (ov > bv || (ov == bv && oi < bi)) { bv = ov; bi = oi; }
-    }
+    for (int i = 1; i < 4; ++i)
+      if (dgr[i] > bv) { bv = dgr[i]; bi = lane + 32 * i; }
+    const uint32_t key = bv > 0.f ? __float_as_uint(bv) : 0u;  // order-preserving for v > 0
+    const uint32_t kmax = __reduce_max_sync(kFull, key);
+    const int p = (int)__reduce_min_sync(kFull, key == kmax ? (uint32_t)bi : 0xffffffffu);
+    bv = __uint_as_float(kmax);
     if (kf == 0) ptol = (float)d * 5.96e-8f * bv;
     if (!(bv > ptol)) break;  // identical decision in every warp
-    const int p = bi;
     const float rs = rsqrtf(bv);
     float* Fk = Xs + kf * kHJLd;
     if (lane == (p & 31)) {
       const int ip = p >> 5;
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const float v = ip == 0 ? x[j][0] : ip == 1 ? x[j][1] : ip == 2 ? x[j][2] : x[j][3];
-        Fk[cj[j]] = (elim >> j) & 1u ? 0.f : v * rs;
+        const float v = ip == 0 ? x[j][0].x : ip == 1 ? x[j][0].y : ip == 2 ? x[j][1].x : x[j][1].y;
+        Fk[cj(j)] = (elim >> j) & 1u ? 0.f : v * rs;
       }
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (cj[j] == p) elim |= 1u << j;
-    __syncthreads();
+      if (cj(j) == p) elim |= 1u << j;
+    __syncthreads();  // F[:, k] complete (the next step writes another column: no second barrier)
     float lr[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) lr[i] = Fk[lane + 32 * i];
+    for (int i = 0; i < 4; ++i) {
+      lr[i] = Fk[lane + 32 * i];
+      dgr[i] = lane + 32 * i == p ? -CUDART_INF_F : fmaf(-lr[i], lr[i], dgr[i]);
+    }
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if ((elim >> j) & 1u) continue;  // warp-uniform
-      const float lc = Fk[cj[j]];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) x[j][i] = fmaf(-lr[i], lc, x[j][i]);
+      const float lc = -Fk[cj(j)];
+      const float2 m = make_float2(lc, lc);
+      x[j][0] = __ffma2_rn(make_float2(lr[0], lr[1]), m, x[j][0]);
+      x[j][1] = __ffma2_rn(make_float2(lr[2], lr[3]), m, x[j][1]);
     }
-    if (tid < d) {
-      const float dv = dg[tid];
-      dg[tid] = tid == p ? -CUDART_INF_F : fmaf(-Fk[tid], Fk[tid], dv);
-    }
-    __syncthreads();
   }
   // append the remaining columns (in index order) after the kf pivot columns
   {
     uint32_t rem[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) rem[i] = __ballot_sync(kFull, dg[lane + 32 * i] != -CUDART_INF_F);
+    for (int i = 0; i < 4; ++i) rem[i] = __ballot_sync(kFull, dgr[i] != -CUDART_INF_F);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if ((elim >> j) & 1u) continue;
-      const int c = cj[j], wd = c >> 5;
+      const int c = cj(j), wd = c >> 5;
       int pos = kf + __popc(rem[wd] & ((1u << (c & 31)) - 1u));
 #pragma unroll
       for (int i = 0; i < 4; ++i) pos += i < wd ? __popc(rem[i]) : 0;
       float* dst = Xs + pos * kHJLd + lane;
 #pragma unroll
-      for (int i = 0; i < 4; ++i) dst[32 * i] = x[j][i];
+      for (int i = 0; i < 4; ++i) dst[32 * i] = xel(x, j, i);
     }
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const float* src = Xs + cj[j] * kHJLd + lane;
+    const float* src = Xs + cj(j) * kHJLd + lane;
 #pragma unroll
-    for (int i = 0; i < 4; ++i) x[j][i] = src[32 * i];
+    for (int i = 0; i < 4; ++i) xel(x, j, i) = src[32 * i];
   }
   __syncthreads();
   hj_norms(x, nrm, dsc, lane);
@@ -381,7 +370,7 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
         float* dst = Xs + (8 * (j < 8 ? ba : bb) + (j & 7)) * kHJLd + lane;
         const float sc = dsc[j];
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) dst[32 * kk] = x[j][kk] * sc;
+        for (int kk = 0; kk < 4; ++kk) dst[32 * kk] = xel(x, j, kk) * sc;
       }
       __syncthreads();
       const int k1 = k == 14 ? 0 : k + 1;
@@ -390,7 +379,7 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
       for (int j = 0; j < 16; ++j) {
         const float* src = Xs + (8 * (j < 8 ? na : nb) + (j & 7)) * kHJLd + lane;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) x[j][kk] = src[32 * kk];
+        for (int kk = 0; kk < 4; ++kk) xel(x, j, kk) = src[32 * kk];
       }
       __syncthreads();
       hj_norms(x, nrm, dsc, lane);
@@ -416,7 +405,7 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
     const float inv = n2 > 0.f ? rsqrtf(n2) : 0.f;
     float* dst = Xs + col * kHJLd + lane;
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk) dst[32 * kk] = x[j][kk] * inv;
+    for (int kk = 0; kk < 4; ++kk) dst[32 * kk] = xel(x, j, kk) * inv;
     if (lane == 0) lam_out[(size_t)u * d + col] = n2 * unscale;  // ||f_j||^2 = lambda_j
   }
   degenerate = __syncthreads_or(degenerate);

@@ -74,7 +74,7 @@ int launch_state_finalize(int nS, int d, bool center, bool weight, const double*
                           cudaStream_t st);
 int launch_finalize(int U, int N, int d, bool center, const CalibWs& ws, cudaStream_t st,
                     const int32_t* nvu = nullptr);
-int launch_jacobi(int U, int d, bool fp64, bool twosided, const CalibWs& ws, cudaStream_t st);
+int launch_jacobi(int U, int d, int r, bool fp64, bool twosided, const CalibWs& ws, cudaStream_t st);
 int launch_select_gather(int U, int d, int r, bool fp64_vecs, bool bf16x2, bool center,
                          const CalibWs& ws, float* R, float* dmu, float* eigvals,
                          uint32_t* mask, int32_t* idx, float* R_full, int32_t* info,

@@ -114,8 +114,12 @@ def test_null_columns(rk, solver):
     assert (cal["info"].cpu().numpy() == 0).all()
     _check(cal, ref, cfg.rank, range(cfg.units))
     Rf = to_np64(cal["R_full"])
-    for u in range(cfg.units):  # the full basis stays orthonormal through the fallback
-        assert np.linalg.norm(Rf[u].T @ Rf[u] - np.eye(cfg.head_dim)) <= 1e-3, u
+    # the full basis stays orthonormal through the fallback; with the default solver a unit
+    # re-solved by the two-sided kernel keeps its fp32 basis outside the r + 8 refined
+    # columns (rotatek.h, R_full)
+    tol = 1e-3 if solver == "twosided" else 5e-3
+    for u in range(cfg.units):
+        assert np.linalg.norm(Rf[u].T @ Rf[u] - np.eye(cfg.head_dim)) <= tol, u
 
 
 @pytest.mark.parametrize("solver", ["onesided", "twosided"])
