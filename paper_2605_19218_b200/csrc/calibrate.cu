@@ -1049,7 +1049,7 @@ int launch_jacobi(int U, int d, int r, bool fp64, bool twosided, const CalibWs& 
     cudaFuncSetAttribute(jacobi32p_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
     // default: one-sided Jacobi in registers; units it cannot normalise (info -2: a null
     // column) are re-solved by the two-sided kernel, which every other unit skips
-    if (!twosided && launch_hestenes(U, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 1e-3f, 30, st) < 0) return -1;
+    if (!twosided && launch_hestenes(U, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 3e-3f, 30, st) < 0) return -1;
     jacobi32p_kernel<128><<<U, kJPThreads, smp, st>>>(ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30,
                                                       twosided ? 0 : 1);
   } else {

@@ -75,6 +75,19 @@ __device__ __forceinline__ float warp_reduce_scatter(const float (&v)[N], int la
   return r;
 }
 
+// Single-instruction MUFU approximations (flush-to-zero: no denormal fix-up code; the
+// operands here are normal or the pair is not rotated)
+__device__ __forceinline__ float rcp_ftz(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float y;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // Columns (0..15 = block A cols 0..7, block B cols 0..7) of pair j in sub-round s.
 //   intra-block: 7 rounds of the circle method on each block's 8 columns (pairs j = 4b + m);
 //   cross-block: pair j = (A_j, B_{(j + s) mod 8}), 8 rounds.
@@ -112,44 +125,46 @@ __device__ __forceinline__ void hj_subround(float2 (&x)[16][2], float* nrm, floa
   const float al = nrm[p], be = nrm[q], dp = dsc[p], dq = dsc[q];
   const float gam = gy * dp * dq;  // inner product of the true columns
   const float g2 = gam * gam, ab = al * be;
-  if (ab > 1e-36f) cmax = fmaxf(cmax, __fdividef(g2, ab));  // (null columns: info -2 later)
+  // (null columns, ab ~ 0, are reported as info -2 after the sweeps)
+  cmax = fmaxf(cmax, ab > 1e-36f ? g2 * rcp_ftz(ab) : 0.f);
   const bool rot = g2 > tol2 * ab;  // cosine above tol
-  // branch-free (the shuffles below need a converged warp): lanes that do not rotate take
-  // a1 = a2 = t = 0, c = 1 whatever zeta is (gam = 0 gives inf / NaN here, discarded)
-  const float zeta = __fdividef(be - al, 2.f * gam);
+  // branch-free: lanes that do not rotate take a1 = a2 = t = 0, c = 1 whatever zeta is
+  // (gam = 0 gives inf / NaN here, discarded), and every pair is updated -- a zero update
+  // leaves the columns bit-identical, and without a skip branch the unrolled sub-rounds keep
+  // their registers in place (a conditional update forces moves at the merge point)
+  const float zeta = (be - al) * rcp_ftz(2.f * gam);
   const float az = fabsf(zeta);
-  // sqrt(1 + zeta^2) ~ |zeta| beyond 1e18 (zeta^2 would overflow); fast reciprocal and
-  // square root: an inexact t only changes the angle slightly (the sweep goes on until
+  // sqrt(1 + zeta^2) ~ |zeta| beyond 1e18 (zeta^2 would overflow); approximate reciprocal
+  // and square root: an inexact t only changes the angle slightly (the sweep goes on until
   // the cosines are small), an inexact c only rescales the pair (norms are recomputed)
   const float z2 = fmaf(az, az, 1.f);
-  float t = __fdividef(1.f, az + (az < 1e18f ? z2 * rsqrtf(z2) : az));
+  float t = rcp_ftz(az + (az < 1e18f ? z2 * rsqrt_ftz(z2) : az));
   t = rot ? (zeta < 0.f ? -t : t) : 0.f;
-  const float c = rsqrtf(fmaf(t, t, 1.f));
+  const float c = rsqrt_ftz(fmaf(t, t, 1.f));
   // scaled rotation: x = d y per column; x_p <- c (x_p - t x_q), x_q <- c (x_q + t x_p)
   // becomes d <- c d and y_p <- y_p - (t d_q / d_p) y_q, y_q <- y_q + (t d_p / d_q) y_p:
   // two FMAs per element pair instead of four multiply(-add)s
-  const float rq = __fdividef(dq, dp);
-  const float a1 = t * rq, a2 = __fdividef(t, rq);
-  if (__any_sync(kFull, rot)) {  // warp-uniform: skip the update when no pair rotates
-    // every lane has read nrm / dsc (their values fed the vote above) before the update
-    if (rot && (lane & 3) == 0) {
-      nrm[p] = fmaf(-t, gam, al);
-      nrm[q] = fmaf(t, gam, be);
-      dsc[p] = dp * c;
-      dsc[q] = dq * c;
-    }
+  const float rq = dq * rcp_ftz(dp);
+  const float a1 = t * rq, a2 = t * rcp_ftz(rq);
+  // every lane has read nrm / dsc (their values fed the coefficients) before the update
+  __syncwarp();
+  if (rot && (lane & 3) == 0) {
+    nrm[p] = fmaf(-t, gam, al);
+    nrm[q] = fmaf(t, gam, be);
+    dsc[p] = dp * c;
+    dsc[q] = dq * c;
+  }
 #pragma unroll
-    for (int j = 0; j < 8; ++j) {  // pair j's coefficients from its lane group, then its update
-      int pp, qq;
-      hj_pair<kIntra>(S, j, pp, qq);
-      const float c1 = __shfl_sync(kFull, a1, 4 * j), c2 = __shfl_sync(kFull, a2, 4 * j);
-      const float2 m1 = make_float2(-c1, -c1), m2 = make_float2(c2, c2);
+  for (int j = 0; j < 8; ++j) {  // pair j's coefficients from its lane group, then its update
+    int pp, qq;
+    hj_pair<kIntra>(S, j, pp, qq);
+    const float c1 = __shfl_sync(kFull, a1, 4 * j), c2 = __shfl_sync(kFull, a2, 4 * j);
+    const float2 m1 = make_float2(-c1, -c1), m2 = make_float2(c2, c2);
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {  // packed fp32x2 FMAs (FFMA2): two rows per instruction
-        const float2 yp = x[pp][h];
-        x[pp][h] = __ffma2_rn(m1, x[qq][h], yp);
-        x[qq][h] = __ffma2_rn(m2, yp, x[qq][h]);
-      }
+    for (int h = 0; h < 2; ++h) {  // packed fp32x2 FMAs (FFMA2): two rows per instruction
+      const float2 yp = x[pp][h];
+      x[pp][h] = __ffma2_rn(m1, x[qq][h], yp);
+      x[qq][h] = __ffma2_rn(m2, yp, x[qq][h]);
     }
   }
   __syncwarp();
@@ -157,17 +172,20 @@ __device__ __forceinline__ void hj_subround(float2 (&x)[16][2], float* nrm, floa
 
 // exact squared norms of the warp's 16 (unscaled) columns into nrm[0..15], scales to 1
 __device__ __forceinline__ void hj_norms(const float2 (&x)[16][2], float* nrm, float* dsc, int lane) {
-  float v[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float2 a = __ffma2_rn(x[j][1], x[j][1], __fmul2_rn(x[j][0], x[j][0]));
-    v[j] = a.x + a.y;
-  }
-  const float r = warp_reduce_scatter<16>(v, lane);  // column lane >> 1
   __syncwarp();
-  if ((lane & 1) == 0) {
-    nrm[lane >> 1] = r;
-    dsc[lane >> 1] = 1.f;
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {  // two halves of 8 columns: fewer live registers
+    float v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const float2 a = __ffma2_rn(x[8 * h + j][1], x[8 * h + j][1], __fmul2_rn(x[8 * h + j][0], x[8 * h + j][0]));
+      v[j] = a.x + a.y;
+    }
+    const float r = warp_reduce_scatter<8>(v, lane);  // column 8 h + (lane >> 2)
+    if ((lane & 3) == 0) {
+      nrm[8 * h + (lane >> 2)] = r;
+      dsc[8 * h + (lane >> 2)] = 1.f;
+    }
   }
   __syncwarp();
 }
