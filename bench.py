@@ -531,7 +531,7 @@ def run_ours(args):
                         (per_layer_us["calibrate"] + per_layer_us["compress"]) * 1e-6), 1),
                     "compress_gbs_1pass_bytes": round(cb / (per_layer_us["compress"] * 1e-6) / 1e9, 1)}
 
-        full = {"solver": "parallel Jacobi (fp32) + fp64 refinement (north_star; eigh arm P:653)"}
+        full = {"solver": "one-sided Jacobi on a pivoted-Cholesky factor (fp32, registers) + fp64 refinement of the r + 8 leading columns on DMMA (north_star; eigh arm P:653)"}
         full.update(full_path(lambda ly: rk.calibrate(ly["K"], ly["Qw"], cfg.rank, ws=calws,
                                                       stream=stream)))
         sub = {"solver": "Cholesky-QR subspace iteration, T=5 (paper default, NEXT-1)"}
