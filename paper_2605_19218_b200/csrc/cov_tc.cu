@@ -16,7 +16,8 @@
 //   llava_b32 (ncu): 290 us (one CTA per unit) -> 214 -> 229 (r1 final) -> 218 (16 epilogue
 //   warps of 32 columns, TMEM released as soon as a window is in registers, no divisions in
 //   the finalize) -> 191 (column sums folded into the Gram MMA instead of 8 extra N = 16 MMAs
-//   per chunk); 512-token windows 167 us but less precise (see kWin).  (fp32 TwoSum
+//   per chunk) -> 178 (only the 10 blocks on/above the diagonal drained, mirrored writes);
+//   512-token windows 167 us but less precise (see kWin).  (fp32 TwoSum
 //   pairs instead of F2F.F64.F32 + DADD in the drain: 203 us, register spills -- not kept.)
 //
 // Warp roles (576 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
@@ -46,8 +47,9 @@ constexpr int kStageBytes = 3 * kHalfBytes;
 constexpr int kEpiWarps = 16;               // 4 per TMEM lane quadrant, 32 accumulator columns each
 constexpr int kThreads = (2 + kEpiWarps) * 32;
 constexpr int kSmem = kStages * kStageBytes + 1024 + 256;
+constexpr int kAcc = 2;                    // TMEM accumulators (3 measured: no change; a = gw & 1)
 constexpr int kAccCols = 256;              // TMEM columns per accumulation window (144 used)
-constexpr int kTmemCols = 512;             // 2 windows x kAccCols (128 Gram + 16 column-sum columns used)
+constexpr int kTmemCols = 512;             // kAcc windows x kAccCols (128 Gram + 16 column-sum columns used)
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_constant__ CUtensorMap tmap, int N,
@@ -62,8 +64,8 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
   uint64_t* full = reinterpret_cast<uint64_t*>(sm + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
   uint64_t* tfull = empty + kStages;
-  uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* tempty = tfull + kAcc;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAcc);
   __shared__ double colsum_sm[kDc];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
       mbar_init(&full[s], gathered ? 32 : 1);
       mbar_init(&empty[s], 1);  // released by the MMA commit alone (no smem column-sum pass)
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kAcc; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], kEpiWarps);
     }
@@ -177,6 +179,12 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     const int q = warp & 3;        // TMEM lane quadrant this warp may access
     const int h = e >> 2;          // accumulator column quarter
     const int row = 32 * q + lane;  // output row (channel i)
+    // S is symmetric: the 6 blocks below the diagonal (column quarter < row quadrant) are
+    // not drained -- their warps only arrive on the TMEM barrier (and the column-quarter-0
+    // ones read the column sums) -- and each warp above the diagonal writes its block AND
+    // the mirrored one (a transposed write is still coalesced: lanes = consecutive columns).
+    // 10 of 16 blocks pass through the fp32 -> fp64 drain, the conversion-bound stage.
+    const bool lower = h < q;
     const int et = e * 32 + lane;   // 0..511
     constexpr int kEpiThreads = kEpiWarps * 32;
     int gi = 0, gw = 0;  // running chunk / window counters (as the producer and MMA warps)
@@ -196,20 +204,30 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
       mbar_wait(&tfull[a], wph);
       ++gw;
       tc::fence_after();
-      const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * kAccCols + h * 32;
-      uint32_t r[2][16], rc = 0;
-      if (h == 0) tc::ld_32x32b_x1(tmem + ((uint32_t)(32 * q) << 16) + a * kAccCols + 128, rc);
+      const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + a * kAccCols;
+      if (!lower) {
+        uint32_t r[2][16], rc = 0;
+        if (h == 0) tc::ld_32x32b_x1(tq + 128, rc);
 #pragma unroll
-      for (int b = 0; b < 2; ++b) tc::ld_32x32b_x16(taddr + b * 16, r[b]);
-      tc::ld_wait();
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&tempty[a]);  // the registers hold the window: free TMEM
+        for (int b = 0; b < 2; ++b) tc::ld_32x32b_x16(tq + h * 32 + b * 16, r[b]);
+        tc::ld_wait();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[a]);  // the registers hold the window: free TMEM
 #pragma unroll
-      for (int b = 0; b < 2; ++b)
+        for (int b = 0; b < 2; ++b)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) acc[b * 16 + j] += (double)__uint_as_float(r[b][j]);
-      if (h == 0) csum += (double)__uint_as_float(rc);
+          for (int j = 0; j < 16; ++j) acc[b * 16 + j] += (double)__uint_as_float(r[b][j]);
+        if (h == 0) csum += (double)__uint_as_float(rc);
+      } else {
+        uint32_t rc = 0;
+        if (h == 0) tc::ld_32x32b_x1(tq + 128, rc);
+        tc::ld_wait();
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&tempty[a]);
+        if (h == 0) csum += (double)__uint_as_float(rc);
+      }
     }
     if (h == 0) colsum_sm[row] = csum;
     asm volatile("bar.sync 1, %0;" ::"r"(kEpiThreads) : "memory");
@@ -220,21 +238,39 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
       const double inv_nu = 1.0 / nu;
       const double mur = center ? colsum_sm[row] * inv_nu : 0.0;
       const double sr = sg[row];
-      double* cqr = cq + (size_t)u * kDc * kDc + (size_t)row * kDc + h * 32;
+      double* cqu = cq + (size_t)u * kDc * kDc;
+      if (!lower) {
+        double* cqr = cqu + (size_t)row * kDc + h * 32;
+        double* cqt = cqu + (size_t)(h * 32) * kDc + row;  // mirrored block, column `row`
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const int c0 = h * 32 + j;
-        const double m0 = center ? colsum_sm[c0] * inv_nu : 0.0;
-        const double m1 = center ? colsum_sm[c0 + 1] * inv_nu : 0.0;
-        const double v0 = sr * sg[c0] * (acc[j] - nu * mur * m0);
-        const double v1 = sr * sg[c0 + 1] * (acc[j + 1] - nu * mur * m1);
-        *reinterpret_cast<double2*>(cqr + j) = make_double2(v0, v1);
+        for (int j = 0; j < 32; j += 2) {
+          const int c0 = h * 32 + j;
+          const double m0 = center ? colsum_sm[c0] * inv_nu : 0.0;
+          const double m1 = center ? colsum_sm[c0 + 1] * inv_nu : 0.0;
+          const double v0 = sr * sg[c0] * (acc[j] - nu * mur * m0);
+          const double v1 = sr * sg[c0 + 1] * (acc[j + 1] - nu * mur * m1);
+          *reinterpret_cast<double2*>(cqr + j) = make_double2(v0, v1);
+          if (h != q) {
+            cqt[(size_t)j * kDc] = v0;
+            cqt[(size_t)(j + 1) * kDc] = v1;
+          }
+        }
       }
       if (et < kDc) mu[(size_t)u * kDc + et] = center ? colsum_sm[et] / nu : 0.0;
     } else {
-      double* out = covpart + ((size_t)u * parts + p) * kDc * kDc + (size_t)row * kDc + h * 32;
+      double* outu = covpart + ((size_t)u * parts + p) * kDc * kDc;
+      if (!lower) {
+        double* out = outu + (size_t)row * kDc + h * 32;
+        double* outt = outu + (size_t)(h * 32) * kDc + row;
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
+        for (int j = 0; j < 32; j += 2) {
+          *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
+          if (h != q) {
+            outt[(size_t)j * kDc] = acc[j];
+            outt[(size_t)(j + 1) * kDc] = acc[j + 1];
+          }
+        }
+      }
       if (et < kDc) colpart[((size_t)u * parts + p) * kDc + et] = colsum_sm[et];
     }
     // every epilogue warp is done reading colsum_sm before the next item's drain may
