@@ -138,8 +138,9 @@ size_t rotatek_workspace_bytes(const rotatek_dims* dims, rotatek_op op);
  *            ~1e-4 per entry for a unit re-solved by the two-sided kernel after a null
  *            C_q column)
  *   info     [U] int32: 0 ok; s > 0 not converged after s sweeps (results are
- *            still written); -1 non-finite input (R, dmu zero-filled, mask 0,
- *            idx -1) (nullable)
+ *            still written; the environment variable ROTATEK_JACOBI_MAX_SWEEPS=<n>,
+ *            read at every call, lowers the sweep caps for fault injection); -1
+ *            non-finite input (R, dmu zero-filled, mask 0, idx -1) (nullable)
  * Errors: NULL, DIMS, ALIGN, WORKSPACE, UNSUPPORTED (d > 256), CUDA.
  */
 rotatek_status rotatek_calibrate(const rotatek_dims* dims, uint32_t flags, const void* K,

@@ -1032,12 +1032,22 @@ int refine_tc_candidates(int d, int r);
 int launch_refine_tc(int U, int kc, const double* cq, const float* v32, float* lam, double* vecs,
                      const int32_t* jinfo, cudaStream_t st);
 
+// Sweep caps (fp32 solvers 30, fp64 40).  ROTATEK_JACOBI_MAX_SWEEPS=<n> lowers them: fault
+// injection for the non-convergence path (info = sweeps > 0, results still written), read at
+// every call.
+static int sweep_cap(int dflt) {
+  const char* e = getenv("ROTATEK_JACOBI_MAX_SWEEPS");
+  const int v = e ? atoi(e) : 0;
+  return v > 0 && v < dflt ? v : dflt;
+}
+
 int launch_jacobi(int U, int d, int r, bool fp64, bool twosided, const CalibWs& ws, cudaStream_t st) {
+  const int cap32 = sweep_cap(30), cap64 = sweep_cap(40);
   if (fp64) {
     size_t sm = jacobi_smem_bytes(d, true);
     cudaFuncSetAttribute(jacobi_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     jacobi_kernel<double><<<U, kJacobiThreads, sm, st>>>(d, ws.cq, ws.lam, (double*)ws.vecs,
-                                                         ws.jinfo, 1e-13, 40);
+                                                         ws.jinfo, 1e-13, cap64);
     return cudaPeekAtLastError() == cudaSuccess ? 1 : -1;
   }
   // fp32 solve into ws.v32, then the fp64 refinement writes the fp64 basis into ws.vecs;
@@ -1049,12 +1059,12 @@ int launch_jacobi(int U, int d, int r, bool fp64, bool twosided, const CalibWs& 
     cudaFuncSetAttribute(jacobi32p_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
     // default: one-sided Jacobi in registers; units it cannot normalise (info -2: a null
     // column) are re-solved by the two-sided kernel, which every other unit skips
-    if (!twosided && launch_hestenes(U, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 3e-3f, 30, st) < 0) return -1;
-    jacobi32p_kernel<128><<<U, kJPThreads, smp, st>>>(ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30,
+    if (!twosided && launch_hestenes(U, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 3e-3f, cap32, st) < 0) return -1;
+    jacobi32p_kernel<128><<<U, kJPThreads, smp, st>>>(ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, cap32,
                                                       twosided ? 0 : 1);
   } else {
     cudaFuncSetAttribute(jacobi32_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    jacobi32_kernel<0><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, 30);
+    jacobi32_kernel<0><<<U, kJ32Threads, sm, st>>>(d, ws.cq, ws.lam, v32, ws.jinfo, 2e-6f, cap32);
   }
   if (cudaPeekAtLastError() != cudaSuccess) return -1;
   // fp64 refinement: on the fp64 tensor cores for the r + 8 leading columns (refine_tc.cu)

@@ -42,8 +42,7 @@ namespace rk {
 namespace {
 constexpr int kHJWarps = 8;
 constexpr int kHJThreads = 32 * kHJWarps;
-constexpr int kHJLd = 129;  // column stride of the exchange buffer (floats): conflict-free
-                            // column writes (lanes = rows) and transposed reads
+constexpr int kHJLd = 130;  // column stride of the exchange buffer (floats, even: float2 rows)
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kNeedTwoSided = -2;
 
@@ -196,6 +195,13 @@ __device__ __forceinline__ float& xel(float2 (&x)[16][2], int j, int k) {
   return (k & 1) ? x[j][k >> 1].y : x[j][k >> 1].x;
 }
 
+// Shared-memory position (floats) of row r within a column: rows (l, l + 32) and
+// (l + 64, l + 96) are adjacent, so a lane moves its x[j][h] as one 8-byte access
+__device__ __forceinline__ int hj_f(int r) { return 2 * ((r & 31) + 32 * (r >> 6)) + ((r >> 5) & 1); }
+__device__ __forceinline__ float2* hj_col2(float* Xs, int col) {
+  return reinterpret_cast<float2*>(Xs + col * kHJLd);
+}
+
 // block held in tournament slot i at block-round k (circle method, slot 0 fixed)
 __device__ __forceinline__ int hj_slot_block(int i, int k) { return i == 0 ? 0 : 1 + (i - 1 + k) % 15; }
 
@@ -292,6 +298,8 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
   // of every warp writes its columns' entries), A <- A - F[:, k] F[:, k]^T on the remaining
   // columns.  Pivots below d eps max_i(C_ii) stop the factorisation; the remaining (tiny)
   // Schur-complement columns are appended to F as they are, so F F^T = C_q up to rounding.
+  // (F[:, k] is column p of A: the symmetric update keeps A exactly symmetric, so the r1-style
+  // row write by lane p % 32 of every warp and this owner-warp column write are the same.)
   // The remaining diagonal is tracked in registers, redundantly by every warp (lane l holds
   // rows l + 32 i), so a step needs a single barrier: the pivot column's publication.
   float dgr[4];
@@ -316,31 +324,44 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
     if (!(bv > ptol)) break;  // identical decision in every warp
     const float rs = rsqrtf(bv);
     float* Fk = Xs + kf * kHJLd;
-    if (lane == (p & 31)) {
-      const int ip = p >> 5;
+    {
+      // F[:, k] = A[:, p] / sqrt(A_pp): column p lives in one warp's registers (blocks w and
+      // 15 - w); that warp writes it (two 8-byte stores per lane), rows already eliminated
+      // as exact zeros
+      const int pb = p >> 3;
+      if (w == (pb < 8 ? pb : 15 - pb)) {
+        const int jp = (pb < 8 ? 0 : 8) + (p & 7);
+        float2 c0 = x[0][0], c1 = x[0][1];
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const float v = ip == 0 ? x[j][0].x : ip == 1 ? x[j][0].y : ip == 2 ? x[j][1].x : x[j][1].y;
-        Fk[cj(j)] = (elim >> j) & 1u ? 0.f : v * rs;
+        for (int j = 1; j < 16; ++j)
+          if (j == jp) { c0 = x[j][0]; c1 = x[j][1]; }
+        c0 = __fmul2_rn(c0, make_float2(rs, rs));
+        c1 = __fmul2_rn(c1, make_float2(rs, rs));
+        if (dgr[0] == -CUDART_INF_F) c0.x = 0.f;
+        if (dgr[1] == -CUDART_INF_F) c0.y = 0.f;
+        if (dgr[2] == -CUDART_INF_F) c1.x = 0.f;
+        if (dgr[3] == -CUDART_INF_F) c1.y = 0.f;
+        float2* F2 = hj_col2(Xs, kf) + lane;
+        F2[0] = c0;
+        F2[32] = c1;
       }
     }
 #pragma unroll
     for (int j = 0; j < 16; ++j)
       if (cj(j) == p) elim |= 1u << j;
     __syncthreads();  // F[:, k] complete (the next step writes another column: no second barrier)
-    float lr[4];
+    const float2 l01 = reinterpret_cast<const float2*>(Fk)[lane];
+    const float2 l23 = reinterpret_cast<const float2*>(Fk)[lane + 32];
+    const float lr[4] = {l01.x, l01.y, l23.x, l23.y};  // rows lane + 32 i
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      lr[i] = Fk[lane + 32 * i];
-      dgr[i] = lane + 32 * i == p ? -CUDART_INF_F : fmaf(-lr[i], lr[i], dgr[i]);
-    }
+    for (int i = 0; i < 4; ++i) dgr[i] = lane + 32 * i == p ? -CUDART_INF_F : fmaf(-lr[i], lr[i], dgr[i]);
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
       if ((elim >> j) & 1u) continue;  // warp-uniform
-      const float lc = -Fk[cj(j)];
+      const float lc = -Fk[hj_f(cj(j))];
       const float2 m = make_float2(lc, lc);
-      x[j][0] = __ffma2_rn(make_float2(lr[0], lr[1]), m, x[j][0]);
-      x[j][1] = __ffma2_rn(make_float2(lr[2], lr[3]), m, x[j][1]);
+      x[j][0] = __ffma2_rn(l01, m, x[j][0]);
+      x[j][1] = __ffma2_rn(l23, m, x[j][1]);
     }
   }
   // append the remaining columns (in index order) after the kf pivot columns
@@ -355,17 +376,17 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
       int pos = kf + __popc(rem[wd] & ((1u << (c & 31)) - 1u));
 #pragma unroll
       for (int i = 0; i < 4; ++i) pos += i < wd ? __popc(rem[i]) : 0;
-      float* dst = Xs + pos * kHJLd + lane;
-#pragma unroll
-      for (int i = 0; i < 4; ++i) dst[32 * i] = xel(x, j, i);
+      float2* dst = hj_col2(Xs, pos) + lane;
+      dst[0] = x[j][0];
+      dst[32] = x[j][1];
     }
   }
   __syncthreads();
 #pragma unroll
   for (int j = 0; j < 16; ++j) {
-    const float* src = Xs + cj(j) * kHJLd + lane;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) xel(x, j, i) = src[32 * i];
+    const float2* src = hj_col2(Xs, cj(j)) + lane;
+    x[j][0] = src[0];
+    x[j][1] = src[32];
   }
   __syncthreads();
   hj_norms(x, nrm, dsc, lane);
@@ -385,19 +406,19 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
       const int ba = hj_slot_block(w, k), bb = hj_slot_block(15 - w, k);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        float* dst = Xs + (8 * (j < 8 ? ba : bb) + (j & 7)) * kHJLd + lane;
+        float2* dst = hj_col2(Xs, 8 * (j < 8 ? ba : bb) + (j & 7)) + lane;
         const float sc = dsc[j];
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) dst[32 * kk] = xel(x, j, kk) * sc;
+        dst[0] = __fmul2_rn(x[j][0], make_float2(sc, sc));
+        dst[32] = __fmul2_rn(x[j][1], make_float2(sc, sc));
       }
       __syncthreads();
       const int k1 = k == 14 ? 0 : k + 1;
       const int na = hj_slot_block(w, k1), nb = hj_slot_block(15 - w, k1);
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const float* src = Xs + (8 * (j < 8 ? na : nb) + (j & 7)) * kHJLd + lane;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) xel(x, j, kk) = src[32 * kk];
+        const float2* src = hj_col2(Xs, 8 * (j < 8 ? na : nb) + (j & 7)) + lane;
+        x[j][0] = src[0];
+        x[j][1] = src[32];
       }
       __syncthreads();
       hj_norms(x, nrm, dsc, lane);
@@ -421,16 +442,16 @@ __global__ void __launch_bounds__(kHJThreads, 2) hestenes_kernel(const double* _
     const float n2 = nrm[j];
     if (!(n2 >= 1e-30f)) degenerate = 1;
     const float inv = n2 > 0.f ? rsqrtf(n2) : 0.f;
-    float* dst = Xs + col * kHJLd + lane;
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) dst[32 * kk] = xel(x, j, kk) * inv;
+    float2* dst = hj_col2(Xs, col) + lane;
+    dst[0] = __fmul2_rn(x[j][0], make_float2(inv, inv));
+    dst[32] = __fmul2_rn(x[j][1], make_float2(inv, inv));
     if (lane == 0) lam_out[(size_t)u * d + col] = n2 * unscale;  // ||f_j||^2 = lambda_j
   }
   degenerate = __syncthreads_or(degenerate);
   float* Vo = vecs + (size_t)u * d * d;
   for (int e = tid; e < d * d; e += kHJThreads) {
     const int row = e / d, col = e % d;
-    Vo[e] = Xs[col * kHJLd + row];
+    Vo[e] = Xs[col * kHJLd + hj_f(row)];
   }
   if (tid == 0)
     jinfo[u] = degenerate ? kNeedTwoSided

@@ -135,3 +135,26 @@ def test_rank_deficient(rk, solver):
     ref = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
     assert (cal["info"].cpu().numpy() == 0).all()
     _check(cal, ref, cfg.rank, range(cfg.units))
+
+
+@pytest.mark.parametrize("solver,fp64", [("onesided", False), ("twosided", False), ("onesided", True)])
+def test_nonconvergence_reported(rk, solver, fp64, monkeypatch):
+    """Fault injection (SURVEY §5 failure detection): ROTATEK_JACOBI_MAX_SWEEPS=1 caps every
+    Jacobi solver at one sweep; info reports the sweeps done (> 0) for every unit and the
+    outputs are still written (finite).  The cap is read at every call: lifting it restores
+    info 0."""
+    import torch
+    cfg = CONFIGS["llava_b1"].with_(h_kv=3, n_vis=300, n_text=0)
+    w = make_workload(cfg, dist="gap")
+    K, Qw = to_torch(w["K"]), to_torch(w["Qw"])
+    flags = _flags(rk, solver) | (rk.EIG_FP64 if fp64 else 0)
+    monkeypatch.setenv("ROTATEK_JACOBI_MAX_SWEEPS", "1")
+    cal = rk.calibrate(K, Qw, cfg.rank, flags)
+    torch.cuda.synchronize()
+    assert cal["info"].cpu().tolist() == [1] * cfg.units
+    assert torch.isfinite(cal["R"]).all() and torch.isfinite(cal["dmu"]).all()
+    assert ((cal["idx"] >= 0) & (cal["idx"] < cfg.head_dim)).all()
+    monkeypatch.delenv("ROTATEK_JACOBI_MAX_SWEEPS")
+    cal = rk.calibrate(K, Qw, cfg.rank, flags)
+    torch.cuda.synchronize()
+    assert (cal["info"].cpu().numpy() == 0).all()

@@ -18,7 +18,7 @@ for cfg in ${CFGS-llava_b32 qwen_b32_r32 joint_b64 long_b16}; do
   [ -n "$KEEP_REP" ] || rm -f gpurun_out/prof_decode_${cfg}_${tag}.ncu-rep   # gpurun_out/ must stay < 64 MiB
 done
 if [ -z "$SKIP_PREFILL" ]; then
-  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cov_tc|compress_tc|jacobi32p|refine|select_gather|subspace" -c 7 \
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:"cov_tc|compress_tc|hestenes|refine|select_gather|subspace" -c 7 \
     -o gpurun_out/prof_prefill_llava_b32_${tag} -f \
     python tools/prof_calib.py llava_b32 > gpurun_out/ncu_prefill_${tag}.log 2>&1
   ncu -i gpurun_out/prof_prefill_llava_b32_${tag}.ncu-rep --page details --csv > gpurun_out/ncu_prefill_llava_b32_${tag}_details.csv 2>/dev/null
