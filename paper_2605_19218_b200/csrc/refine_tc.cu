@@ -63,6 +63,14 @@ __global__ void __launch_bounds__(kRtThreads, 1) refine_tc_kernel(const double* 
   if (jinfo[u] == -1) return;  // non-finite input: select zero-fills the unit
   const double* C = cq + (size_t)u * d * d;
   float* lu = lam + (size_t)u * d;
+  // this lane's A fragments of step (1), C[8w + g][4i + c], requested before anything else so
+  // their latency hides behind the ranking and the V0 staging (32 loads in flight per lane)
+  double ca[d / 4];
+  {
+    const double* Crow = C + (size_t)(8 * w + g) * d + c;
+#pragma unroll
+    for (int i = 0; i < d / 4; ++i) ca[i] = __ldg(Crow + 4 * i);
+  }
 
   // rank of every column by lambda0 (descending; ties -> lower index): sort-free and exact
   if (tid < d) l0[tid] = (double)lu[tid];
@@ -80,6 +88,7 @@ __global__ void __launch_bounds__(kRtThreads, 1) refine_tc_kernel(const double* 
   __syncthreads();
   // V0 (fp32, row-major, solver order) -> shared fp64, columns permuted
   const float* V0u = v0g + (size_t)u * d * d;
+#pragma unroll
   for (int e = tid; e < d * d / 4; e += kRtThreads) {
     const float4 v = __ldg(reinterpret_cast<const float4*>(V0u) + e);
     const int x = (4 * e) / d, o = (4 * e) % d;
@@ -97,10 +106,9 @@ __global__ void __launch_bounds__(kRtThreads, 1) refine_tc_kernel(const double* 
     double acc[NT][2];
 #pragma unroll
     for (int nt = 0; nt < NT; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
-    const double* Crow = C + (size_t)(8 * w + g) * d + c;
-#pragma unroll 4
+#pragma unroll
     for (int k0 = 0; k0 < d; k0 += 4) {
-      const double a = __ldg(Crow + k0);
+      const double a = ca[k0 / 4];
       const double* Vk = V0 + (k0 + c) * LDA + g;
 #pragma unroll
       for (int nt = 0; nt < NT; ++nt) dmma884(acc[nt], a, Vk[8 * nt]);
