@@ -16,8 +16,9 @@
 //   llava_b32 (ncu): 290 us (one CTA per unit) -> 214 -> 229 (r1 final) -> 218 (16 epilogue
 //   warps of 32 columns, TMEM released as soon as a window is in registers, no divisions in
 //   the finalize) -> 191 (column sums folded into the Gram MMA instead of 8 extra N = 16 MMAs
-//   per chunk) -> 178 (only the 10 blocks on/above the diagonal drained, mirrored writes);
-//   512-token windows 167 us but less precise (see kWin).  (fp32 TwoSum
+//   per chunk) -> 178 (only the 10 blocks on/above the diagonal drained, mirrored writes)
+//   -> 165 (every block drained again, all written transposed: coalesced stores, see the
+//   epilogue); 512-token windows 167 us but less precise (see kWin).  (fp32 TwoSum
 //   pairs instead of F2F.F64.F32 + DADD in the drain: 203 us, register spills -- not kept.)
 //
 // Warp roles (576 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
@@ -34,7 +35,16 @@ namespace rk {
 namespace {
 constexpr int kTK = 128;                 // tokens per chunk (fp32 accumulation window)
 constexpr int kDc = 128;                 // head dim
-constexpr int kStages = 4;  // 6 measured slower (254 vs 229 us, llava_b32)
+#ifndef COV_STAGES
+#define COV_STAGES 4
+#endif
+#ifdef COV_DIAG_NOFIN
+constexpr bool kDiagNoFin = true;  // diagnostics build only: no finalize / partial writes
+#else
+constexpr bool kDiagNoFin = false;
+#endif
+// 2, 3 and 4 stages measured equal (r2, tools/run_covdiag.sh); 6 slower (254 vs 229 us)
+constexpr int kStages = COV_STAGES;
 // chunks per fp32 TMEM accumulation window: 256 tokens (SURVEY E-6).  512 was measured (r2,
 // tools/cov_err2.py): 191 -> 167 us on llava_b32 (half the fp32 -> fp64 drains), but the worst
 // unit's projector error vs the fp64 oracle on large-mean planted-gap keys grows 9.7e-5 ->
@@ -162,7 +172,11 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
           for (int kk = 0; kk < kTK / 16; ++kk) {
             // MN-major, SWIZZLE_128B: LBO = next 64-channel half, SBO = next 8-token group
             const uint64_t desc = tc::smem_desc(base + kk * 16 * 128, kHalfBytes, 1024, tc::SWZ_128B);
+#ifndef COV_DIAG_NOMMA  // diagnostics build only: stream without the Gram MMAs
             tc::mma_bf16(tmem + a * kAccCols, desc, desc, idesc, (first && kk == 0) ? 0u : 1u);
+#else
+            (void)desc;
+#endif
           }
           tc::commit(&empty[s]);
           if (last) {
@@ -179,12 +193,16 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     const int q = warp & 3;        // TMEM lane quadrant this warp may access
     const int h = e >> 2;          // accumulator column quarter
     const int row = 32 * q + lane;  // output row (channel i)
-    // S is symmetric: the 6 blocks below the diagonal (column quarter < row quadrant) are
-    // not drained -- their warps only arrive on the TMEM barrier (and the column-quarter-0
-    // ones read the column sums) -- and each warp above the diagonal writes its block AND
-    // the mirrored one (a transposed write is still coalesced: lanes = consecutive columns).
-    // 10 of 16 blocks pass through the fp32 -> fp64 drain, the conversion-bound stage.
-    const bool lower = h < q;
+    // Output: each warp writes its 32 x 32 block TRANSPOSED -- lane = row i of the block,
+    // stores go to C[32h + j][32q + lane], so every store instruction covers 32 consecutive
+    // doubles (256 B).  S = K^T K is symmetric (D[i][j] and D[j][i] are the same products
+    // summed in the same order), so the transposed block is block (h, q) of S, and every
+    // block is written exactly once.  Row-major stores from this layout put the lanes 1 KB
+    // apart (32 sectors per instruction): 178 -> 165 us on llava_b32 (ncu).  Measured and not
+    // kept (tools/run_covdiag*.sh): draining only the 10 blocks on/above the diagonal with the
+    // other 6 written from a shared-memory staging (166 us); 2 or 3 ring stages (equal); a
+    // third TMEM accumulator (equal).  The ablations put the rest above the pure TMA stream
+    // (111 us, 6.8 TB/s) into the fp64 drain and the per-unit finalize.
     const int et = e * 32 + lane;   // 0..511
     constexpr int kEpiThreads = kEpiWarps * 32;
     int gi = 0, gw = 0;  // running chunk / window counters (as the producer and MMA warps)
@@ -205,72 +223,45 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
       ++gw;
       tc::fence_after();
       const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16) + a * kAccCols;
-      if (!lower) {
-        uint32_t r[2][16], rc = 0;
-        if (h == 0) tc::ld_32x32b_x1(tq + 128, rc);
+      uint32_t r[2][16], rc = 0;
+      if (h == 0) tc::ld_32x32b_x1(tq + 128, rc);
 #pragma unroll
-        for (int b = 0; b < 2; ++b) tc::ld_32x32b_x16(tq + h * 32 + b * 16, r[b]);
-        tc::ld_wait();
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[a]);  // the registers hold the window: free TMEM
+      for (int b = 0; b < 2; ++b) tc::ld_32x32b_x16(tq + h * 32 + b * 16, r[b]);
+      tc::ld_wait();
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[a]);  // the registers hold the window: free TMEM
+#ifndef COV_DIAG_NODRAIN  // diagnostics build only: skip the fp64 accumulation
 #pragma unroll
-        for (int b = 0; b < 2; ++b)
+      for (int b = 0; b < 2; ++b)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[b * 16 + j] += (double)__uint_as_float(r[b][j]);
-        if (h == 0) csum += (double)__uint_as_float(rc);
-      } else {
-        uint32_t rc = 0;
-        if (h == 0) tc::ld_32x32b_x1(tq + 128, rc);
-        tc::ld_wait();
-        tc::fence_before();
-        __syncwarp();
-        if (lane == 0) tc::mbar_arrive(&tempty[a]);
-        if (h == 0) csum += (double)__uint_as_float(rc);
-      }
+        for (int j = 0; j < 16; ++j) acc[b * 16 + j] += (double)__uint_as_float(r[b][j]);
+#else
+      acc[0] += (double)__uint_as_float(r[0][0] ^ r[1][15]);
+#endif
+      if (h == 0) csum += (double)__uint_as_float(rc);
     }
     if (h == 0) colsum_sm[row] = csum;
     asm volatile("bar.sync 1, %0;" ::"r"(kEpiThreads) : "memory");
-    if (fused) {
+    if (fused && !kDiagNoFin) {
       // parts == 1: this CTA saw every token of the unit -> finalize here (mu, C, C_q)
       const double* sg = sigma + (size_t)u * kDc;
       const double nu = (double)tsrc.valid(u, N);  // tokens of the unit (per-unit lengths)
       const double inv_nu = 1.0 / nu;
       const double mur = center ? colsum_sm[row] * inv_nu : 0.0;
       const double sr = sg[row];
-      double* cqu = cq + (size_t)u * kDc * kDc;
-      if (!lower) {
-        double* cqr = cqu + (size_t)row * kDc + h * 32;
-        double* cqt = cqu + (size_t)(h * 32) * kDc + row;  // mirrored block, column `row`
+      double* cqt = cq + (size_t)u * kDc * kDc + (size_t)(h * 32) * kDc + row;  // column `row`
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          const int c0 = h * 32 + j;
-          const double m0 = center ? colsum_sm[c0] * inv_nu : 0.0;
-          const double m1 = center ? colsum_sm[c0 + 1] * inv_nu : 0.0;
-          const double v0 = sr * sg[c0] * (acc[j] - nu * mur * m0);
-          const double v1 = sr * sg[c0 + 1] * (acc[j + 1] - nu * mur * m1);
-          *reinterpret_cast<double2*>(cqr + j) = make_double2(v0, v1);
-          if (h != q) {
-            cqt[(size_t)j * kDc] = v0;
-            cqt[(size_t)(j + 1) * kDc] = v1;
-          }
-        }
+      for (int j = 0; j < 32; ++j) {
+        const int c0 = h * 32 + j;
+        const double m0 = center ? colsum_sm[c0] * inv_nu : 0.0;
+        cqt[(size_t)j * kDc] = sr * sg[c0] * (acc[j] - nu * mur * m0);
       }
       if (et < kDc) mu[(size_t)u * kDc + et] = center ? colsum_sm[et] / nu : 0.0;
-    } else {
-      double* outu = covpart + ((size_t)u * parts + p) * kDc * kDc;
-      if (!lower) {
-        double* out = outu + (size_t)row * kDc + h * 32;
-        double* outt = outu + (size_t)(h * 32) * kDc + row;
+    } else if (!kDiagNoFin) {
+      double* outt = covpart + ((size_t)u * parts + p) * kDc * kDc + (size_t)(h * 32) * kDc + row;
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          *reinterpret_cast<double2*>(out + j) = make_double2(acc[j], acc[j + 1]);
-          if (h != q) {
-            outt[(size_t)j * kDc] = acc[j];
-            outt[(size_t)(j + 1) * kDc] = acc[j + 1];
-          }
-        }
-      }
+      for (int j = 0; j < 32; ++j) outt[(size_t)j * kDc] = acc[j];
       if (et < kDc) colpart[((size_t)u * parts + p) * kDc + et] = colsum_sm[et];
     }
     // every epilogue warp is done reading colsum_sm before the next item's drain may
