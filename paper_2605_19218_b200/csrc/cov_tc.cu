@@ -18,7 +18,8 @@
 //   the finalize) -> 191 (column sums folded into the Gram MMA instead of 8 extra N = 16 MMAs
 //   per chunk) -> 178 (only the 10 blocks on/above the diagonal drained, mirrored writes)
 //   -> 165 (every block drained again, all written transposed: coalesced stores, see the
-//   epilogue); 512-token windows 167 us but less precise (see kWin).  (fp32 TwoSum
+//   epilogue) -> 160 (per-column finalize factors staged in shared memory once per unit:
+//   0.80 of the copy peak); 512-token windows 167 us but less precise (see kWin).  (fp32 TwoSum
 //   pairs instead of F2F.F64.F32 + DADD in the drain: 203 us, register spills -- not kept.)
 //
 // Warp roles (576 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA issuer,
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
   uint64_t* tempty = tfull + kAcc;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + kAcc);
   __shared__ double colsum_sm[kDc];
+  __shared__ double2 fac_sm[kDc];  // fused finalize: (s_c, s_c mu_c n) per column
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // PERSISTENT: this CTA takes the work items (u, p) = blockIdx.x, + gridDim.x, ...; the ring
@@ -244,20 +246,26 @@ __global__ void __launch_bounds__(kThreads, 1) cov_tc_kernel(const __grid_consta
     if (h == 0) colsum_sm[row] = csum;
     asm volatile("bar.sync 1, %0;" ::"r"(kEpiThreads) : "memory");
     if (fused && !kDiagNoFin) {
-      // parts == 1: this CTA saw every token of the unit -> finalize here (mu, C, C_q)
-      const double* sg = sigma + (size_t)u * kDc;
+      // parts == 1: this CTA saw every token of the unit -> finalize here (mu, C, C_q):
+      //   C_q[r][c] = s_r s_c (S_rc - n mu_r mu_c) = (s_r s_c) S_rc - (s_r mu_r)(s_c mu_c n)
+      // with the per-column factors (s_c, s_c mu_c n) staged in shared memory once per unit
       const double nu = (double)tsrc.valid(u, N);  // tokens of the unit (per-unit lengths)
       const double inv_nu = 1.0 / nu;
-      const double mur = center ? colsum_sm[row] * inv_nu : 0.0;
-      const double sr = sg[row];
+      if (et < kDc) {
+        const double m = center ? colsum_sm[et] * inv_nu : 0.0;
+        const double sgc = sigma[(size_t)u * kDc + et];
+        fac_sm[et] = make_double2(sgc, sgc * m * nu);
+        mu[(size_t)u * kDc + et] = center ? colsum_sm[et] / nu : 0.0;
+      }
+      asm volatile("bar.sync 1, %0;" ::"r"(kEpiThreads) : "memory");
+      const double2 fr = fac_sm[row];
+      const double sr = fr.x, srm = fr.y * inv_nu;  // s_r, s_r mu_r
       double* cqt = cq + (size_t)u * kDc * kDc + (size_t)(h * 32) * kDc + row;  // column `row`
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const int c0 = h * 32 + j;
-        const double m0 = center ? colsum_sm[c0] * inv_nu : 0.0;
-        cqt[(size_t)j * kDc] = sr * sg[c0] * (acc[j] - nu * mur * m0);
+        const double2 fc = fac_sm[h * 32 + j];
+        cqt[(size_t)j * kDc] = fma(sr * fc.x, acc[j], -srm * fc.y);
       }
-      if (et < kDc) mu[(size_t)u * kDc + et] = center ? colsum_sm[et] / nu : 0.0;
     } else if (!kDiagNoFin) {
       double* outt = covpart + ((size_t)u * parts + p) * kDc * kDc + (size_t)(h * 32) * kDc + row;
 #pragma unroll
