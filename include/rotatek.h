@@ -75,10 +75,12 @@ enum {
   ROTATEK_QUERY_WEIGHT = 1u << 1, /* C_q = (sigma sigma^T) (.) C.  Off (or
                                      W == 0): sigma == 1, the K-only PCA arm   */
   ROTATEK_EIG_FP64 = 1u << 2,     /* run the whole Jacobi eigensolver in fp64 (always on for
-                                     fp32 caches).  Default for bf16 caches: fp32 parallel
-                                     Jacobi followed by one fp64 refinement step
+                                     fp32 caches).  Default for bf16 caches: an fp32 Jacobi
+                                     solve (d = 128: one-sided, on a pivoted-Cholesky factor
+                                     of C_q) followed by one fp64 refinement step
                                      (B = V0^T C_q V0, lambda = diag B, V = V0 (I + W) with
-                                     the first-order correction W_ij = B_ij / (B_jj - B_ii)) */
+                                     the first-order correction W_ij = B_ij / (B_jj - B_ii)),
+                                     for d = 128 and r <= 64 on the r + 8 leading columns */
   ROTATEK_EIG_TWOSIDED = 1u << 3, /* d = 128, fp32 solve: use the two-sided packed-triangle
                                      Jacobi (A and V in shared memory) instead of the default
                                      one-sided (Hestenes) Jacobi on C_q with the columns in

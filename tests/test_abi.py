@@ -174,3 +174,14 @@ def test_token_prefill_host_validation(rk):
     d64 = rk.make_dims(4, 1, 64, 16, 300, 0, 32, rk.BF16)      # d != 128
     assert cal(d64) == rk.ERR_UNSUPPORTED
     assert cmp(d64) == rk.ERR_UNSUPPORTED
+
+
+def test_flag_values_match_header(rk):
+    """The binding's flag constants are the header's enum values (a mismatch would silently
+    select another solver or drop the centering)."""
+    src = open(HEADER).read()
+    flags = {m.group(1): 1 << int(m.group(2))
+             for m in re.finditer(r"ROTATEK_([A-Z0-9_]+)\s*=\s*1u\s*<<\s*(\d+)\s*,", src)}
+    for name in ("CENTER", "QUERY_WEIGHT", "EIG_FP64", "EIG_TWOSIDED", "SIMT_ONLY"):
+        assert getattr(rk, name) == flags[name], name
+    assert rk.DEFAULT_FLAGS == flags["CENTER"] | flags["QUERY_WEIGHT"]
