@@ -1176,12 +1176,23 @@ __global__ void __launch_bounds__(128) select_gather_kernel(
   if (mask) for (int w = tid; w < words; w += blockDim.x) mask[(size_t)u * words + w] = mask_sm[w];
   if (idx) for (int k = tid; k < r; k += blockDim.x) idx[(size_t)u * r + k] = kidx_sm[k];
   const TV* Vu = vecs + (size_t)u * d * d;
-  for (int e = tid; e < d * r; e += blockDim.x) {
-    const int x = e / r, k = e % r;
-    float v = (float)Vu[(size_t)x * d + kidx_sm[k]];
-    (void)bf16x2;  // R is stored as plain fp32 (RNE of the solver value)
-    Rs[e] = v;
-    R[(size_t)u * d * r + e] = v;
+  (void)bf16x2;  // R is stored as plain fp32 (RNE of the solver value)
+  {
+    // thread -> one kept column k (its solver column read once), rows x0, x0 + xs, ...: the
+    // global loads do not depend on shared-memory traffic inside the loop, so they pipeline
+    // (one (x, k) per iteration with the index reloaded from shared memory serialized them:
+    // ~40 us per unit, latency-bound at small U)
+    const int xs = (int)blockDim.x / r;  // r <= d <= blockDim.x
+    if (tid < xs * r) {
+      const int k = tid % r, col = kidx_sm[k];
+      float* Ru = R + (size_t)u * d * r;
+#pragma unroll 4
+      for (int x = tid / r; x < d; x += xs) {
+        const float v = (float)Vu[(size_t)x * d + col];
+        Rs[x * r + k] = v;
+        Ru[x * r + k] = v;
+      }
+    }
   }
   if (R_full)
     for (int e = tid; e < d * d; e += blockDim.x) R_full[(size_t)u * d * d + e] = (float)Vu[e];

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests -m gpu -q -k "calibrate or select or full_size or end_to_end or mode or offline or token or eig or subspace" > gpurun_out/gputest_sel.log 2>&1; echo "pytest rc $?" >> gpurun_out/gputest_sel.log
+for c in qwen_b1_r32 llava_b32; do
+  timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"select" --csv python tools/prof_calib.py $c > gpurun_out/sel_launches_$c.csv 2>&1
+done
