@@ -3,33 +3,38 @@
 // the working matrix held in REGISTERS.
 //
 // C_q is symmetric positive semi-definite (C is a Gram matrix of centered keys and
-// (sigma sigma^T) (.) C is PSD by the Schur product theorem), so its singular vectors are its
-// eigenvectors.  Starting from X = C_q (V = I), plane rotations X <- X J_pq make the columns of
-// X mutually orthogonal: then X = C_q V with V orthogonal and X^T X = V^T C_q^2 V diagonal, so
-// X = V diag(lambda) column by column and the normalised columns ARE the eigenvectors (for a
-// PSD matrix the sign ambiguity of an SVD does not arise).  V itself is never stored.
+// (sigma sigma^T) (.) C is PSD by the Schur product theorem).  The kernel first factors
+// C_q = F F^T by a diagonally pivoted Cholesky (below), then makes the columns of X = F
+// mutually orthogonal by plane rotations X <- X J_pq: X = F V with V orthogonal and
+// X X^T = F F^T = C_q, so once X^T X is diagonal the normalised columns of X are C_q's
+// eigenvectors and ||x_j||^2 its eigenvalues.  V itself is never stored.  (Without the
+// factorisation, X = C_q also works -- its singular vectors are its eigenvectors -- but the
+// working Gram matrix then has C_q^2's spectrum: 10.6 instead of ~6 sweeps.)
 //
 // Why one-sided on B200: the two-sided kernel (jacobi32p_kernel, calibrate.cu) must touch
 // rows AND columns of A every round, so A and V live in shared memory and every round moves
 // every element through the shared-memory pipe (ncu: L1/shared 78-91 %), 11.5 ms for LLaVA
 // b32.  A column rotation needs only its two columns: here warp w holds 2 blocks of 8 columns
-// with lane l owning rows l, l+32, l+64, l+96 (64 fp32 registers), every pair of columns a warp
-// holds is rotated in registers, and the only cross-lane traffic is the pair's inner product
-// (a butterfly reduce-scatter of 8 partial sums per 8 disjoint pairs) and the broadcast of
-// (c, s).  Blocks move between warps through shared memory once per block-round (15 per
-// sweep, a 2-block tournament over 16 blocks; every column pair meets once per sweep).
+// with lane l owning rows l, l+32 and l+64, l+96 as two float2 (64 fp32 registers; rotations
+// run as packed FFMA2), every pair of columns a warp holds is rotated in registers, and the
+// only cross-lane traffic is the pair's inner product (a butterfly reduce-scatter of 8 partial
+// sums per 8 disjoint pairs) and the broadcast of the rotation coefficients.  Blocks move
+// between warps through shared memory once per block-round (15 per sweep, a 2-block
+// tournament over 16 blocks; every column pair meets once per sweep).
 //
 // Rotation (Golub & Van Loan 8.4, the same Schur rotation as the two-sided kernels, applied to
 // the 2x2 Gram matrix [[a, g], [g, b]] of columns p, q):
 //   zeta = (b - a) / (2 g),  t = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)),  c = 1/sqrt(1+t^2),
-//   x_p <- c x_p - s x_q,  x_q <- s x_p + c x_q (s = t c),  a <- a - t g,  b <- b + t g.
-// A pair is rotated only when |g| > tol sqrt(a b) (its cosine exceeds tol); a sweep without a
-// rotation ends the iteration.  Column norms are recomputed exactly after every exchange.
+//   x_p <- c x_p - s x_q,  x_q <- s x_p + c x_q (s = t c),  a <- a - t g,  b <- b + t g,
+// applied in scaled form (hj_subround).  A pair is rotated when its cosine |g|/sqrt(a b)
+// exceeds tol (2e-6); the iteration stops after a sweep whose largest cosine is below qstop
+// (3e-3: convergence is quadratic, so the cosines left are O(qstop^2)).  Column norms are
+// recomputed exactly after every exchange.
 //
 // Output: V0 = X diag(1/||x_j||) (fp32, [d][d] row-major, columns in solver order) and
-// lambda_j = ||x_j||; the fp64 refinement (refine_smem_kernel) follows as for the two-sided
-// solver.  A column whose squared norm falls below 1e-30 ||C_q||_F^2 (an exactly or nearly
-// null direction, whose normalisation is undefined) marks the unit info = -2 and the
+// lambda_j = ||x_j||^2; the fp64 refinement (refine_tc_kernel, or refine_smem_kernel for
+// r > 64) follows.  A column whose squared norm falls below 1e-30 ||C_q||_F^2 (an exactly or
+// nearly null direction, whose normalisation is undefined) marks the unit info = -2 and the
 // two-sided kernel re-solves it (launch_jacobi).
 #include <cstdio>
 #include <cstdlib>
