@@ -36,7 +36,12 @@ struct CmpCfg {
   static constexpr int B_SPLIT = 2 * B_HALF;                // both channel halves
   static constexpr int B_BYTES = 3 * B_SPLIT;               // hi, mid, lo
   static constexpr int TMEM_COLS = (2 * RK <= 32) ? 32 : (2 * RK <= 64) ? 64 : (2 * RK <= 128) ? 128 : 256;
-  static constexpr int SMEM = kStages * kStageBytes + B_BYTES + 1024 + 256;
+  // r <= 32: the epilogue stages each warp's 32 output rows (32 x r bf16) in shared memory and
+  // writes them as one contiguous block (r = 64 / 128 would not fit two CTAs per SM)
+  static constexpr bool STAGE_OUT = RK <= 32;
+  static constexpr int CPR = RK / 8;                       // 16-byte chunks per output row
+  static constexpr int OUT_BYTES = STAGE_OUT ? 4 * 32 * RK * 2 : 0;
+  static constexpr int SMEM = kStages * kStageBytes + B_BYTES + 1024 + 256 + OUT_BYTES;
 };
 
 __device__ __forceinline__ uint16_t bf16_bits_rn(float x) {
@@ -58,6 +63,7 @@ __global__ void __launch_bounds__(kThreads, 2) compress_tc_kernel(const __grid_c
   uint64_t* tfull = empty + kStages;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint4* outsm = reinterpret_cast<uint4*>(Bsm + C::B_BYTES + 256);  // [4 warps][32 rows][CPR]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.y, p = blockIdx.x;
@@ -165,6 +171,10 @@ __global__ void __launch_bounds__(kThreads, 2) compress_tc_kernel(const __grid_c
       const uint32_t taddr = tmem + ((uint32_t)(32 * q) << 16) + a * RK;
       const int tok = (t_lo + i) * kTM + m;
       __nv_bfloat16* dst = Kc + ((size_t)u * N + tok) * RK;
+      // chunk swizzle of a staged row: the 8 rows one 128-byte shared-memory phase touches
+      // land in 8 distinct 16-byte bank groups for the row-wise writes and the block reads
+      auto swz = [](int row) { return (row / (8 / C::CPR)) & (C::CPR - 1); };
+      uint4* stg = outsm + (warp - 2) * 32 * C::CPR;
 #pragma unroll
       for (int b = 0; b < RK / 16; ++b) {
         uint32_t r[16];
@@ -175,11 +185,28 @@ __global__ void __launch_bounds__(kThreads, 2) compress_tc_kernel(const __grid_c
         for (int j = 0; j < 8; ++j)
           pk[j] = (uint32_t)bf16_bits_rn(__uint_as_float(r[2 * j])) |
                   ((uint32_t)bf16_bits_rn(__uint_as_float(r[2 * j + 1])) << 16);
-        if (tok < N) {
+        if constexpr (C::STAGE_OUT) {
+          stg[lane * C::CPR + ((2 * b) ^ swz(lane))] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          stg[lane * C::CPR + ((2 * b + 1) ^ swz(lane))] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
+        } else if (tok < N) {
           uint4* d4 = reinterpret_cast<uint4*>(dst + b * 16);
           d4[0] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
           d4[1] = make_uint4(pk[4], pk[5], pk[6], pk[7]);
         }
+      }
+      if constexpr (C::STAGE_OUT) {
+        // the warp's 32 tokens are 32 consecutive rows of K~: one contiguous block, written
+        // with every lane on consecutive 16-byte chunks (rows written lane-per-row put the
+        // lanes r x 2 bytes apart)
+        __syncwarp();
+        const int tok0 = tok - lane;
+        uint4* g4 = reinterpret_cast<uint4*>(Kc + ((size_t)u * N + tok0) * RK);
+#pragma unroll
+        for (int c = lane; c < 32 * C::CPR; c += 32) {
+          const int row = c / C::CPR, ch = c % C::CPR;
+          if (tok0 + row < N) g4[c] = stg[row * C::CPR + (ch ^ swz(row))];
+        }
+        __syncwarp();  // reads done before the next tile's staging
       }
       tc::fence_before();
       __syncwarp();
