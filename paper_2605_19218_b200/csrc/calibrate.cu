@@ -14,28 +14,49 @@ namespace rk {
 // ============================================================== step 1: sigma
 // sigma[u][j] = sqrt(sum_{g,w} Qw[u][g][w][j]^2) in fp64 (reading Q4: pooled over
 // the G query heads of the unit).  sigma == 1 when !weight or W == 0.
+// Threads (j, part): channel j, rows part, part + 4, ... with two accumulators each, then the
+// four partial sums added in part order (deterministic).  (One thread per channel walking all
+// G x W rows was a 224-long dependent chain for Qwen: ~18 us per launch at any U.)
+constexpr int kSigParts = 4;
 template <typename T>
 __global__ void sigma_kernel(int G, int W, int d, bool weight, const T* __restrict__ Qw,
                              double* __restrict__ sigma) {
+  __shared__ double part_ss[kSigParts][256];
   const int u = blockIdx.x;
-  for (int j = threadIdx.x; j < d; j += blockDim.x) {
-    double ss = 0.0;
-    if (weight && W > 0) {
-      const T* base = Qw + (size_t)u * G * W * d + j;
-      for (int row = 0; row < G * W; ++row) {
-        double x = Elem<T>::to_d(base[(size_t)row * d]);
-        ss = fma(x, x, ss);
+  const int dp = blockDim.x / kSigParts;  // channels per pass (>= d for d <= 256)
+  const int j = threadIdx.x % dp, part = threadIdx.x / dp;
+  const int rows = G * W;
+  if (weight && W > 0) {
+    double s0 = 0.0, s1 = 0.0;
+    if (j < d) {
+      const T* base = Qw + (size_t)u * rows * d + j;
+      int row = part;
+      for (; row + kSigParts < rows; row += 2 * kSigParts) {
+        const double x0 = Elem<T>::to_d(base[(size_t)row * d]);
+        const double x1 = Elem<T>::to_d(base[(size_t)(row + kSigParts) * d]);
+        s0 = fma(x0, x0, s0);
+        s1 = fma(x1, x1, s1);
       }
-      sigma[(size_t)u * d + j] = sqrt(ss);
-    } else {
-      sigma[(size_t)u * d + j] = 1.0;
+      if (row < rows) {
+        const double x0 = Elem<T>::to_d(base[(size_t)row * d]);
+        s0 = fma(x0, x0, s0);
+      }
+      part_ss[part][j] = s0 + s1;
     }
+    __syncthreads();
+    if (part == 0 && j < d) {
+      double ss = 0.0;
+      for (int p2 = 0; p2 < kSigParts; ++p2) ss += part_ss[p2][j];
+      sigma[(size_t)u * d + j] = sqrt(ss);
+    }
+  } else if (part == 0 && j < d) {
+    sigma[(size_t)u * d + j] = 1.0;
   }
 }
 
 int launch_sigma(int U, int G, int W, int d, bool bf16, bool weight, const void* Qw,
                  double* sigma, cudaStream_t st) {
-  int th = d < 128 ? 32 * ((d + 31) / 32) : 128;
+  const int th = kSigParts * 32 * ((d + 31) / 32);  // d <= 256: <= 1024 threads
   if (bf16)
     sigma_kernel<__nv_bfloat16><<<U, th, 0, st>>>(G, W, d, weight,
                                                   (const __nv_bfloat16*)Qw, sigma);
