@@ -211,7 +211,9 @@ def calibrate(K: torch.Tensor, Qw: torch.Tensor | None, rank: int, flags: int = 
     """Alg. 1 steps 1-5 (+ select, delta_mu).  K [U, N, d]; Qw [U, G, W, d] or None.
     tok_idx [U, n] int32: calibrate on rows tok_idx[u] of K [U, n_src, d] (token pruning
     survivors, gathered by the kernel); n_vis_u [U] int32: per-unit valid token counts
-    (rotatek_calibrate_tokens).
+    (rotatek_calibrate_tokens).  flags: CENTER | QUERY_WEIGHT (default), EIG_FP64 (fp64
+    Jacobi), EIG_TWOSIDED (two-sided instead of the default one-sided fp32 Jacobi, d = 128),
+    SIMT_ONLY (CUDA-core covariance) -- include/rotatek.h.
 
     Returns dict(R [U,d,r] f32, dmu [U,d] f32, eigvals [U,d] f32, mask [U,ceil(d/32)] i32
     (uint32 bit pattern), idx [U,r] i32, info [U] i32, R_full [U,d,d] f32 if want_full)."""
