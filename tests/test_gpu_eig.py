@@ -158,3 +158,18 @@ def test_nonconvergence_reported(rk, solver, fp64, monkeypatch):
     cal = rk.calibrate(K, Qw, cfg.rank, flags)
     torch.cuda.synchronize()
     assert (cal["info"].cpu().numpy() == 0).all()
+
+
+@pytest.mark.parametrize("rank", [8, 64, 100, 128])
+def test_refinement_paths(rank, rk):
+    """The fp64 refinement behind the one-sided solver takes the DMMA candidate kernel for
+    r + 8 <= 72 (KC = 40 / 72) and the all-column kernel above; planted gap at r, G-cal gates
+    (r = d = 128: every column kept, R_r is the full basis)."""
+    import torch
+    cfg = CONFIGS["llava_b1"].with_(h_kv=3, n_vis=400, n_text=0, rank=rank)
+    w = make_workload(cfg, dist="gap")
+    cal = rk.calibrate(to_torch(w["K"]), to_torch(w["Qw"]), cfg.rank, want_full=True)
+    torch.cuda.synchronize()
+    ref = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
+    assert (cal["info"].cpu().numpy() == 0).all()
+    _check(cal, ref, cfg.rank, range(cfg.units), projector=rank < cfg.head_dim)
