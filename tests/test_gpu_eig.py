@@ -173,3 +173,27 @@ def test_refinement_paths(rank, rk):
     ref = orc.calibrate(w["K"].f64(), w["Qw"].f64(), cfg.rank)
     assert (cal["info"].cpu().numpy() == 0).all()
     _check(cal, ref, cfg.rank, range(cfg.units), projector=rank < cfg.head_dim)
+
+
+@pytest.mark.parametrize("solver", ["onesided", "twosided"])
+def test_wide_spectrum(rk, solver):
+    """Keys whose last 64 channels are scaled by 1e-4 (C_q eigenvalues spanning ~1e-8 of the
+    largest): the pivoted Cholesky stops at its d eps threshold and the tiny Schur-complement
+    columns ride along; the top-r subspace (planted gap) and every gate still hold."""
+    import torch
+    cfg = CONFIGS["llava_b1"].with_(h_kv=3, n_vis=500, n_text=0)
+    w = make_workload(cfg, dist="gap")
+    K = to_torch(w["K"]).float()
+    K[:, :, 64:] *= 1e-4
+    K = K.to(torch.bfloat16).contiguous()
+    cal = rk.calibrate(K, to_torch(w["Qw"]), cfg.rank, _flags(rk, solver), want_full=True)
+    torch.cuda.synchronize()
+    ref = orc.calibrate(to_np64(K), w["Qw"].f64(), cfg.rank)
+    assert (cal["info"].cpu().numpy() == 0).all()
+    _check(cal, ref, cfg.rank, range(cfg.units), projector=False)
+    R = to_np64(cal["R"])
+    for u in range(cfg.units):  # the kept subspace = the oracle's wherever its gap is clear
+        lam = np.sort(ref["lam"][u])[::-1]
+        rel_gap = (lam[cfg.rank - 1] - lam[cfg.rank]) / lam[0]
+        P, Pref = R[u] @ R[u].T, ref["R"][u] @ ref["R"][u].T
+        assert np.linalg.norm(P - Pref) <= max(1e-3, 1e-7 / rel_gap), (u, rel_gap)
