@@ -118,7 +118,8 @@ size_t rotatek_workspace_bytes(const rotatek_dims* dims, rotatek_op op);
  *   mu      = (1/N) sum_n K_n                     (ROTATEK_CENTER, else 0)
  *   C       = (K - mu)^T (K - mu)                 (no 1/N)
  *   C_q     = (sigma sigma^T) (.) C               (ROTATEK_QUERY_WEIGHT, else C)
- *   C_q     = R diag(lambda) R^T                  (batched parallel Jacobi)
+ *   C_q     = R diag(lambda) R^T                  (batched Jacobi: d = 128 one-sided on a
+ *                                                  pivoted-Cholesky factor + fp64 refinement)
  *   keep    = the r largest lambda, ties -> lower solver index
  *   R_r     = R[:, keep] in ascending index order
  *   dmu     = mu - R_r (R_r^T mu), computed in fp64 from the STORED R_r
